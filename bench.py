@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""All-pairs PRNU PCE benchmark (BASELINE.json configs[1]): pairs/sec on B200.
+
+Workload (`config.workload`): N=4,096 synthetic PRNU-like patterns of
+1024x1024 fp32, all C(N,2) = 8,386,560 pairs through the PCE compare.  One
+step = one full all-pairs job: preprocess every item from its HBM-resident
+parsed pattern into the device slot tier, then every quadtree leaf of this
+rank's share through the fused compare kernels.
+
+  value   pairs/s over all ranks, inputs resident in HBM at the start of the
+          timed region, timed with CUDA events on the engine stream, max over ranks
+  e2e     the same job through the public engine API from pinned HOST patterns,
+          H2D inside the timed region, plus the D2H of the packed result triangle
+  roofline  dominant kernel = one PCE compare batch (pce_corr_cols + pce_rows_reduce)
+  cpu_baseline  the float64 oracle (oracle/pce.py) on a bounded pair sample
+
+`python bench.py --impl reference` times the reference-side CPU path (the
+oracle port; the reference itself has no PCE) on the same workload.
+Multi-GPU: launched under torchrun, leaves are sharded across ranks (strong
+scaling of one job); NCCL is used once, to reduce the result triangle to rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096, help="items (default: configs[1], 4,096)")
+    ap.add_argument("--side", type=int, default=1024, help="pattern side (default 1024)")
+    ap.add_argument("--leaf", type=int, default=16)
+    ap.add_argument("--cameras", type=int, default=64)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    except Exception:
+        return dict(PEAKS_FALLBACK), "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = []
+        smax = None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: float64 oracle on a bounded pair sample (TEST-INFRASTRUCTURE code
+# used only as the timed reference arm, never as the product path).
+
+def _cpu_worker(args):
+    side, seed, cameras, pairs, budget = args
+    import numpy as np
+    from oracle import pce as opce
+    keys = sorted({k for p in pairs for k in p})
+    items = opce.prnu_patterns(side, side, 0, 1, cameras, seed)  # warm imports
+    spectra = {}
+    done = 0
+    t0 = time.perf_counter()
+    for (i, j) in pairs:
+        for k in (i, j):
+            if k not in spectra:
+                spectra[k] = opce.preprocess(opce.prnu_patterns(side, side, k, 1, cameras, seed)[0])
+        opce.compare(spectra[i], spectra[j], side, side)
+        done += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    return done, time.perf_counter() - t0, len(spectra)
+
+
+def cpu_baseline(n, side, cameras, seed, budget_s):
+    """Pairs/s of the float64 oracle over all host cores (one process per core).
+
+    Each worker preprocesses the items of its own pair sample (rfft2 per item,
+    charged to the measured time, like the GPU step's preprocess) and compares
+    pairs until the budget expires."""
+    import multiprocessing as mp
+    import random
+    cores = os.cpu_count() or 1
+    rng = random.Random(seed)
+    # each worker takes a small leaf-like block so items are reused (R ~ 1 within the block)
+    blocks = []
+    for w in range(cores):
+        base = rng.randrange(0, max(1, n - 16))
+        ks = list(range(base, min(n, base + 16)))
+        blocks.append([(a, b) for ai, a in enumerate(ks) for b in ks[ai + 1:]])
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_cpu_worker, [(side, seed, cameras, blk, budget_s) for blk in blocks])
+    wall = time.perf_counter() - t0
+    pairs = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"value": pairs / busy, "unit": "pairs/s", "cores": cores, "kind": "port",
+            "sample": f"{pairs} pairs of {side}x{side} PCE (16-item blocks, rfft2 preprocess included) "
+                      f"on {cores} processes, {busy:.1f}s busy ({wall:.1f}s wall incl. spawn)"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n, side = args.n, args.side
+    pairs_total = n * (n - 1) // 2
+    workload = f"PRNU PCE all-pairs, N={n} patterns of {side}x{side} fp32 (BASELINE configs[1])"
+    metric = "pairs/sec (whole box)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = []
+        cb = None
+        for _ in range(max(1, args.warmup) + args.steps):
+            cb = cpu_baseline(n, side, args.cameras, args.seed, max(3.0, args.cpu_seconds / 3))
+            steps.append(cb["value"])
+        vals = steps[args.warmup:] or steps
+        value = sum(vals) / len(vals)
+        line = {"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * pairs_total / value,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": workload, "n": n, "side": side, "parallelism": f"cpu{cb['cores']}"},
+                "cpu_baseline": dict(cb, value=value),
+                "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_2009_04755_b200 import _lib, device
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    parsed_bytes = side * side * 4
+    items = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
+    device.synth_prnu(side, side, 0, n, args.cameras, args.seed, items)
+    params = _lib.app_params(_lib.APP_PCE, n, height=side, width=side, threshold=60.0)
+    eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=n, rank=rank, world=world)
+    out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
+    estream = torch.cuda.ExternalStream(eng.stream())
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+    eng.reset_stats()
+    eng.set_profiling(every=37, max_samples=4096)
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(estream)
+    kms, ksamples = 0.0, 0
+    for _ in range(args.steps):
+        eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+        a, b = eng.kernel_time()
+        kms += a
+        ksamples += b
+    ev1.record(estream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = eng.stats()
+    my_pairs = st["pairs_done"]
+    t = torch.tensor([ms, float(my_pairs)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms, all_pairs = float(tmax[0]), float(t[1])
+    else:
+        all_pairs = float(my_pairs)
+    value = all_pairs / (ms / 1e3)
+    eng.set_profiling(0)
+
+    # ---- e2e: pinned host patterns -> engine -> packed triangle back on host
+    e2e = None
+    if not args.no_e2e:
+        try:
+            host = torch.empty(n * side * side, dtype=torch.float32, pin_memory=True)
+            host.copy_(items)
+            res_host = torch.empty(pairs_total, dtype=torch.float64, pin_memory=True)
+            del items
+            torch.cuda.empty_cache()
+            eng.run(out, flags, host_items=host, parsed_stride=parsed_bytes)  # warm the H2D path
+            eng.reset_stats()
+            barrier()
+            torch.cuda.synchronize()
+            # events on torch's stream bracket the engine's stream work: rk_engine_run is
+            # synchronous, and the D2H of the results follows it on this stream
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                eng.run(out, flags, host_items=host, parsed_stride=parsed_bytes)
+                if world > 1:
+                    dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)  # disjoint pair ids: exact gather
+                res_host.copy_(out, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ems = e0.elapsed_time(e1)
+            st2 = eng.stats()
+            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt[0])
+            e2e = {"value": all_pairs / (ems / 1e3), "unit": "pairs/s",
+                   "h2d_bytes_per_step": int(st2["h2d_bytes"] // max(1, args.steps)),
+                   "d2h_bytes_per_step": pairs_total * 8}
+        except RuntimeError as exc:  # e.g. pinned-memory exhaustion
+            e2e = {"value": None, "unit": "pairs/s", "error": str(exc)[:200]}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peaks_src = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    batch = eng.params.batch_pairs or 16
+    slot_bytes = side * side * 4
+    alg_bytes_per_pair = 2 * slot_bytes          # two half-spectra per pair
+    roofline = None
+    if ksamples:
+        per_launch_ms = kms / ksamples
+        achieved = alg_bytes_per_pair * batch / (per_launch_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": None,
+                    "kernel": "pce compare batch (pce_corr_cols + pce_rows_reduce)",
+                    "pairs_per_launch": batch, "ms_per_launch": per_launch_ms,
+                    "alg_bytes_per_pair": alg_bytes_per_pair, "peak_source": peaks_src,
+                    "fp32_flops_per_pair": 2 * 5 * (side // 2) * side * math.log2(side)}
+
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline(n, side, args.cameras, args.seed, args.cpu_seconds)
+
+    line = {"metric": metric, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": workload, "n": n, "side": side, "pairs": pairs_total, "leaf_block": args.leaf,
+                       "parallelism": f"pairs{world}", "l2": "inputs (16 GiB patterns + 16 GiB spectra) >> L2"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": st["kernel_launches"],
+            "cache": {"loads": st["loads"], "R": st["loads"] / n / max(1, args.steps) * world,
+                      "device_hits": st["hits"], "device_misses": st["misses"],
+                      "hit_rate": st["hits"] / max(1, st["hits"] + st["misses"])}}
+    print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

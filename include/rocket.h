@@ -1,0 +1,179 @@
+/*
+ * rocket.h -- C ABI of librocket, the B200-native all-pairs compare engine.
+ *
+ * This is the drop-in boundary for the reference's plugin path: the
+ * `allpairs.apps.Application` contract
+ *   /root/reference/pkg/src/allpairs/apps.py:74-125
+ * (path_for_key / fetch_raw / parse / preprocess / compare / postprocess)
+ * and the packed upper-triangle result layout of
+ *   PairLedger.pair_id  /root/reference/pkg/src/allpairs/scheduler.py:228-231
+ *   completion record   /root/reference/pkg/src/allpairs/wire.py:120, :163-181
+ *
+ * Plain pointers and sizes only.  Device pointers are named d_*, host
+ * pointers h_*.  Streams are cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Every entry point returns an rk_status; the message of
+ * the last failure on the calling thread is available from rk_last_error().
+ *
+ * Ownership: slot arenas and output buffers belong to the caller; an rk_app
+ * owns only its constant tables and scratch workspace.  Kernels borrow slot
+ * memory for the stream-ordered duration of a call (the reference's ReadLease
+ * contract, slotcache.py:42-59).  One rk_app may be used by one stream at a
+ * time; create one app per stream for concurrency.
+ */
+#ifndef ROCKET_H
+#define ROCKET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference's exception taxonomy
+ * (/root/reference/pkg/src/allpairs/errors.py). */
+typedef enum {
+  RK_OK = 0,
+  RK_ERR_VALUE = 1,         /* ValueError: i >= j, stage/shape mismatch (apps.py:69-71, :205-206, :335-336) */
+  RK_ERR_MALFORMED = 2,     /* MalformedInput (errors.py:8-9; apps.py:293-298) */
+  RK_ERR_SLOT_OVERFLOW = 3, /* SlotOverflow (errors.py:12-13; apps.py:128-132) */
+  RK_ERR_NO_EVICTABLE = 4,  /* NoEvictableSlot (errors.py:16-20; slotcache.py:276-277) */
+  RK_ERR_DEVICE = 5,        /* AppError: a CUDA call or kernel failed (errors.py:4-5) */
+  RK_ERR_UNSUPPORTED = 6    /* parameter combination not built for sm_100a in this library */
+} rk_status;
+
+/* Application kinds.  SYNTHETIC and CV restate the reference's two built-in
+ * apps (apps.py:154-227, :251-363); PCE / NCC / GMM are the paper's
+ * forensics and microscopy comparisons, absent from the
+ * reference and pinned by the oracle in /root/repo/oracle. */
+typedef enum {
+  RK_APP_SYNTHETIC = 0,
+  RK_APP_CV = 1,
+  RK_APP_PCE = 2,
+  RK_APP_NCC = 3,
+  RK_APP_GMM = 4
+} rk_app_kind;
+
+typedef struct {
+  int32_t kind;          /* rk_app_kind */
+  int32_t n;             /* item count; pair ids are dense over C(n,2) */
+  int32_t height;        /* PCE/NCC: pattern rows */
+  int32_t width;         /* PCE/NCC: pattern columns */
+  uint64_t seed;         /* SYNTHETIC: value = mix64(seed, 0xC0403A3E, i, j) / 2^64 (apps.py:207) */
+  double threshold;      /* postprocess: match = value >= threshold; NaN => match is None */
+  int32_t max_entries;   /* CV: slot capacity in (u64 token, f64 freq) entries; GMM: max localizations */
+  int32_t batch_pairs;   /* pairs per launch (PCE workspace sizing); 0 = default */
+  int32_t gmm_angles;    /* GMM: rotation grid size; 0 = default */
+  float gmm_scale;       /* GMM: Gaussian scale added to per-point sigma^2; 0 = default */
+} rk_app_params;
+
+/* One pair job.  slot_a/slot_b index the caller's slot arena; i < j are the
+ * item keys; the result lands at out[pair_id(i, j)]. */
+typedef struct {
+  int32_t i;
+  int32_t j;
+  int32_t slot_a;
+  int32_t slot_b;
+} rk_pair;
+
+typedef struct rk_app rk_app;
+
+int rk_abi_version(void);
+const char* rk_last_error(void);
+const char* rk_status_name(int status);
+
+/* pair_id(i, j) = i*(2n-i-1)/2 + (j-i-1); -1 when !(0 <= i < j < n).
+ * Restates PairLedger.pair_id (scheduler.py:228-231). */
+int64_t rk_pair_id(int64_t n, int64_t i, int64_t j);
+/* Inverse of rk_pair_id; returns RK_ERR_VALUE when pid is out of range. */
+rk_status rk_pair_from_id(int64_t n, int64_t pid, int64_t* i, int64_t* j);
+
+rk_status rk_app_create(const rk_app_params* params, int device, rk_app** out);
+void rk_app_destroy(rk_app* app);
+/* Bytes of one preprocessed item in its device slot (Application.slot_size). */
+size_t rk_app_slot_bytes(const rk_app* app);
+/* Bytes of one parsed item as handed to rk_preprocess. */
+size_t rk_app_parsed_bytes(const rk_app* app);
+
+/* Application.preprocess for a batch of items already resident on the device
+ * (replaces apps.py:304-318 and the gpu-lane preprocess at engine.py:464-472).
+ * d_parsed: n_items parsed items, parsed_stride bytes apart.
+ * Item k is written to d_slots + h_slot_idx[k]*slot_stride. */
+rk_status rk_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items,
+                        void* d_slots, size_t slot_stride, const int32_t* h_slot_idx,
+                        void* stream);
+
+/* Application.compare + postprocess for a batch of pairs (replaces apps.py:201-208,
+ * :331-358 and the compare dispatch at engine.py:519-548).  Writes
+ * d_out[pair_id] (f64) and, if d_flags != NULL, d_flags[pair_id] with the wire
+ * encoding of PairResult.match: 0 = None, 1 = False, 3 = True (wire.py:165-167). */
+rk_status rk_compare_pairs(rk_app* app, const void* d_slots, size_t slot_stride,
+                           const rk_pair* h_pairs, int n_pairs,
+                           double* d_out, uint8_t* d_flags, void* stream);
+
+/* Quadtree leaf: all pairs (i, j) with i in rows, j in cols and i < j, enumerated
+ * row-major like Region.pairs (scheduler.py:45-48).  h_row_slots/h_col_slots give
+ * the slot of each key. */
+rk_status rk_compare_tile(rk_app* app, const void* d_slots, size_t slot_stride,
+                          int32_t r0, int32_t r1, int32_t c0, int32_t c1,
+                          const int32_t* h_slot_of_key,
+                          double* d_out, uint8_t* d_flags, void* stream);
+
+/* Deterministic synthetic inputs (test/bench data generators, not the hot path). */
+/* PRNU-like patterns: item k = 0.2*K[k % cameras] + N(0,1), fp32, h*w each. */
+rk_status rk_synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras,
+                        uint64_t seed, float* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * All-pairs engine: quadtree tiling (scheduler.py:20-117) over a device slot
+ * table with LRU eviction (slotcache.py:139-282), fed from a pinned host
+ * tier of parsed items with async H2D + preprocess (engine.py:436-508).
+ * ------------------------------------------------------------------------- */
+typedef struct rk_engine rk_engine;
+
+typedef struct {
+  int32_t leaf_block;      /* quadtree leaf side (config.py:73 default 8) */
+  int32_t device_slots;    /* device tier capacity in slots */
+  int32_t streams;         /* compare streams (each owns an rk_app workspace) */
+  int32_t rank;            /* this rank's share of the leaves ... */
+  int32_t world;           /* ... out of world (leaves dealt round-robin in DFS blocks) */
+} rk_engine_params;
+
+typedef struct {
+  int64_t pairs_done;
+  int64_t loads;           /* fresh preprocess executions (engine.py:443-448) */
+  int64_t hits;            /* device tier hits   (slotcache.py:166-170) */
+  int64_t misses;          /* device tier misses (slotcache.py:178-186) */
+  int64_t evictions;
+  int64_t tiles;
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int64_t kernel_launches;
+} rk_engine_stats;
+
+rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,
+                           int device, rk_engine** out);
+void rk_engine_destroy(rk_engine* eng);
+/* Run every pair assigned to this rank.  Parsed items come from host memory
+ * (h_parsed, parsed_stride apart, pinned for async copies) or, when h_parsed is
+ * NULL, from device memory d_parsed.  Results go to d_out/d_flags (device,
+ * C(n,2) entries).  Synchronous on return. */
+rk_status rk_engine_run(rk_engine* eng, const void* h_parsed, const void* d_parsed,
+                        size_t parsed_stride, double* d_out, uint8_t* d_flags);
+rk_status rk_engine_stats_get(const rk_engine* eng, rk_engine_stats* out);
+rk_status rk_engine_reset_stats(rk_engine* eng);
+/* Sample CUDA-event timing of every `every`-th compare batch (0 = off), at most
+ * max_samples per run, on the engine's stream. */
+rk_status rk_engine_set_profiling(rk_engine* eng, int every, int max_samples);
+/* Summed device time and count of the sampled compare batches of the last run. */
+rk_status rk_engine_kernel_time(const rk_engine* eng, double* ms_total, int64_t* samples);
+/* The engine's cudaStream_t (for callers that order their own work after a run). */
+void* rk_engine_stream(const rk_engine* eng);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROCKET_H */

@@ -1,0 +1,155 @@
+"""ctypes binding of librocket (include/rocket.h).
+
+The product path always goes through this library: there is no CPU fallback.
+Importing the package on a machine without the built ``librocket.so`` raises
+immediately, and every failing C call raises the Python exception that the
+reference would raise for the same condition (errors.py taxonomy).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+from .errors import AppError, MalformedInput, NoEvictableSlot, SlotOverflow
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librocket.so")
+
+RK_OK = 0
+RK_ERR_VALUE = 1
+RK_ERR_MALFORMED = 2
+RK_ERR_SLOT_OVERFLOW = 3
+RK_ERR_NO_EVICTABLE = 4
+RK_ERR_DEVICE = 5
+RK_ERR_UNSUPPORTED = 6
+
+APP_SYNTHETIC = 0
+APP_CV = 1
+APP_PCE = 2
+APP_NCC = 3
+APP_GMM = 4
+
+
+class AppParams(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("n", C.c_int32),
+        ("height", C.c_int32),
+        ("width", C.c_int32),
+        ("seed", C.c_uint64),
+        ("threshold", C.c_double),
+        ("max_entries", C.c_int32),
+        ("batch_pairs", C.c_int32),
+        ("gmm_angles", C.c_int32),
+        ("gmm_scale", C.c_float),
+    ]
+
+
+class Pair(C.Structure):
+    _fields_ = [("i", C.c_int32), ("j", C.c_int32), ("slot_a", C.c_int32), ("slot_b", C.c_int32)]
+
+
+class EngineParams(C.Structure):
+    _fields_ = [
+        ("leaf_block", C.c_int32),
+        ("device_slots", C.c_int32),
+        ("streams", C.c_int32),
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+    ]
+
+
+class EngineStats(C.Structure):
+    _fields_ = [
+        ("pairs_done", C.c_int64),
+        ("loads", C.c_int64),
+        ("hits", C.c_int64),
+        ("misses", C.c_int64),
+        ("evictions", C.c_int64),
+        ("tiles", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+        ("kernel_launches", C.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+# (name, restype, argtypes) for every symbol declared in include/rocket.h
+SIGNATURES = [
+    ("rk_abi_version", C.c_int, []),
+    ("rk_last_error", C.c_char_p, []),
+    ("rk_status_name", C.c_char_p, [C.c_int]),
+    ("rk_pair_id", C.c_int64, [C.c_int64, C.c_int64, C.c_int64]),
+    ("rk_pair_from_id", C.c_int, [C.c_int64, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("rk_app_create", C.c_int, [C.POINTER(AppParams), C.c_int, C.POINTER(C.c_void_p)]),
+    ("rk_app_destroy", None, [C.c_void_p]),
+    ("rk_app_slot_bytes", C.c_size_t, [C.c_void_p]),
+    ("rk_app_parsed_bytes", C.c_size_t, [C.c_void_p]),
+    ("rk_preprocess", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_size_t,
+                                C.POINTER(C.c_int32), C.c_void_p]),
+    ("rk_compare_pairs", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Pair), C.c_int,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("rk_compare_tile", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("rk_synth_prnu", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                C.c_void_p, C.c_void_p]),
+    ("rk_engine_create", C.c_int, [C.POINTER(AppParams), C.POINTER(EngineParams), C.c_int,
+                                   C.POINTER(C.c_void_p)]),
+    ("rk_engine_destroy", None, [C.c_void_p]),
+    ("rk_engine_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
+    ("rk_engine_stats_get", C.c_int, [C.c_void_p, C.POINTER(EngineStats)]),
+    ("rk_engine_reset_stats", C.c_int, [C.c_void_p]),
+    ("rk_engine_set_profiling", C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    ("rk_engine_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("rk_engine_stream", C.c_void_p, [C.c_void_p]),
+]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the all-pairs engine has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, restype, argtypes in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = restype
+        fn.argtypes = argtypes
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return (lib.rk_last_error() or b"").decode(errors="replace")
+
+
+def check(status: int) -> None:
+    """Raise the reference's exception type for a failing status."""
+    if status == RK_OK:
+        return
+    msg = last_error()
+    if status == RK_ERR_VALUE:
+        raise ValueError(msg)
+    if status == RK_ERR_MALFORMED:
+        raise MalformedInput(msg)
+    if status == RK_ERR_SLOT_OVERFLOW:
+        raise SlotOverflow(msg)
+    if status == RK_ERR_NO_EVICTABLE:
+        raise NoEvictableSlot(msg)
+    if status == RK_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise AppError(f"librocket device failure: {msg}")
+
+
+def app_params(kind: int, n: int, *, height: int = 0, width: int = 0, seed: int = 0,
+               threshold: float | None = None, max_entries: int = 0, batch_pairs: int = 0,
+               gmm_angles: int = 0, gmm_scale: float = 0.0) -> AppParams:
+    return AppParams(kind, n, height, width, seed & ((1 << 64) - 1),
+                     math.nan if threshold is None else float(threshold),
+                     max_entries, batch_pairs, gmm_angles, gmm_scale)

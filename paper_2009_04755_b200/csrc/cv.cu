@@ -1,0 +1,178 @@
+// CompositionVectorApp on sm_100a: preprocess (count -> frequency) and the
+// sparse k-mer cosine as a warp-per-pair merge-path kernel.
+//
+// Restates /root/reference/pkg/src/allpairs/apps.py:
+//   preprocess  :304-318  freq = count / total   (bit-exact: both ints < 2^53)
+//   compare     :331-354  sorted merge dot / (norm_a * norm_b), 0 if a norm is 0
+//   postprocess :356-358  match = value >= threshold
+// Norms are computed once at preprocess instead of per compare (SURVEY.md
+// appendix: changes only the fp64 summation order, inside the 1e-9 tests).
+//
+// Parsed item (reference byte format, apps.py:299-302): <I dim> + dim x <Q token><I count>.
+// Slot layout (device):  u32 dim | u32 pad | f64 norm | u64 token[cap] | f64 freq[cap]
+#include <math.h>
+
+#include "internal.h"
+
+namespace rk {
+
+namespace {
+
+__device__ __forceinline__ uint32_t ld_u32_unaligned(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+__device__ __forceinline__ uint64_t ld_u64_unaligned(const uint8_t* p) {
+  return (uint64_t)ld_u32_unaligned(p) | ((uint64_t)ld_u32_unaligned(p + 4) << 32);
+}
+
+// One CTA per item.
+__global__ void cv_preprocess_kernel(const uint8_t* __restrict__ parsed, size_t parsed_stride, SlotList dst,
+                                     uint8_t* __restrict__ slots, size_t slot_stride, int cap,
+                                     int* __restrict__ status) {
+  const int item = blockIdx.x;
+  const uint8_t* src = parsed + (size_t)item * parsed_stride;
+  const uint32_t dim = ld_u32_unaligned(src);
+  uint8_t* slot = slots + (size_t)dst.idx[item] * slot_stride;
+  if (dim == 0 || (int64_t)dim > cap) {
+    if (threadIdx.x == 0) atomicMax(status, dim == 0 ? (int)RK_ERR_MALFORMED : (int)RK_ERR_SLOT_OVERFLOW);
+    return;
+  }
+  __shared__ unsigned long long s_total;
+  __shared__ double s_sq;
+  if (threadIdx.x == 0) {
+    s_total = 0ull;
+    s_sq = 0.0;
+  }
+  __syncthreads();
+  unsigned long long tot = 0;
+  for (uint32_t k = threadIdx.x; k < dim; k += blockDim.x) tot += ld_u32_unaligned(src + 4 + 12 * (size_t)k + 8);
+  atomicAdd(&s_total, tot);
+  __syncthreads();
+  const double total = (double)s_total;
+  uint64_t* tok = reinterpret_cast<uint64_t*>(slot + 16);
+  double* freq = reinterpret_cast<double*>(slot + 16 + 8 * (size_t)cap);
+  double sq = 0.0;
+  for (uint32_t k = threadIdx.x; k < dim; k += blockDim.x) {
+    const uint8_t* e = src + 4 + 12 * (size_t)k;
+    const double f = (double)ld_u32_unaligned(e + 8) / total;
+    tok[k] = ld_u64_unaligned(e);
+    freq[k] = f;
+    sq = fma(f, f, sq);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sq, sq);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<uint32_t*>(slot) = dim;
+    *reinterpret_cast<uint32_t*>(slot + 4) = 0u;
+    *reinterpret_cast<double*>(slot + 8) = sqrt(s_sq);
+  }
+}
+
+// Merge-path split: number of A elements among the first `diag` merged
+// elements, where ties go to A first (A[i] <= B[j] takes A).
+__device__ __forceinline__ int merge_path(const uint64_t* a, int na, const uint64_t* b, int nb, int diag) {
+  int lo = max(0, diag - nb), hi = min(diag, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    // take mid A elements and diag-mid B elements: valid if A[mid] > B[diag-mid-1]
+    if (a[mid] <= b[diag - mid - 1]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One warp per pair (8 pairs per CTA).
+__global__ void __launch_bounds__(256) cv_compare_kernel(PairBatch b, const uint8_t* __restrict__ slots,
+                                                         size_t slot_stride, int cap, double* __restrict__ out,
+                                                         uint8_t* __restrict__ flags, double threshold) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 8 + warp;
+  if (p >= b.npairs) return;
+  const uint8_t* sa = slots + (size_t)b.slot_a[p] * slot_stride;
+  const uint8_t* sb = slots + (size_t)b.slot_b[p] * slot_stride;
+  const int na = (int)*reinterpret_cast<const uint32_t*>(sa);
+  const int nb = (int)*reinterpret_cast<const uint32_t*>(sb);
+  const double norm_a = *reinterpret_cast<const double*>(sa + 8);
+  const double norm_b = *reinterpret_cast<const double*>(sb + 8);
+  const uint64_t* ta = reinterpret_cast<const uint64_t*>(sa + 16);
+  const uint64_t* tb = reinterpret_cast<const uint64_t*>(sb + 16);
+  const double* fa = reinterpret_cast<const double*>(sa + 16 + 8 * (size_t)cap);
+  const double* fb = reinterpret_cast<const double*>(sb + 16 + 8 * (size_t)cap);
+  const int total = na + nb;
+  const int per = (total + 31) / 32;
+  const int d0 = min(total, lane * per), d1 = min(total, d0 + per);
+  int i = merge_path(ta, na, tb, nb, d0);
+  int j = d0 - i;
+  const int i_end = merge_path(ta, na, tb, nb, d1);
+  const int j_end = d1 - i_end;
+  double dot = 0.0;
+  // Ties take A first, so when A[i] is consumed the B head is the only
+  // candidate match (tokens are unique and sorted within each item); the head
+  // may already belong to the next lane's segment, which is fine to read.
+  while (i < i_end || j < j_end) {
+    const bool take_a = (i < i_end) && (j >= j_end || ta[i] <= tb[j]);
+    if (take_a) {
+      if (j < nb && tb[j] == ta[i]) dot = fma(fa[i], fb[j], dot);
+      ++i;
+    } else {
+      ++j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) {
+    const double v = (norm_a > 0.0 && norm_b > 0.0) ? dot / (norm_a * norm_b) : 0.0;
+    out[b.pid[p]] = v;
+    if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
+  }
+}
+
+}  // namespace
+
+rk_status cv_init(rk_app* app) {
+  const int cap = app->p.max_entries;
+  if (cap <= 0) return set_error(RK_ERR_VALUE, "CV app needs max_entries > 0");
+  app->slot_bytes = 16 + 16 * (size_t)cap;
+  app->parsed_bytes = 4 + 12 * (size_t)cap;
+  return RK_OK;
+}
+
+rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
+                        size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s) {
+  int* d_status = nullptr;
+  RK_CUDA(cudaMallocAsync(&d_status, sizeof(int), s));
+  RK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  for (int base = 0; base < n_items; base += kMaxBatch) {
+    const int m = n_items - base < kMaxBatch ? n_items - base : kMaxBatch;
+    SlotList dst;
+    dst.n = m;
+    for (int k = 0; k < m; ++k) dst.idx[k] = h_slot_idx[base + k];
+    cv_preprocess_kernel<<<m, 256, 0, s>>>(static_cast<const uint8_t*>(d_parsed) + (size_t)base * parsed_stride,
+                                           parsed_stride, dst, static_cast<uint8_t*>(d_slots), slot_stride,
+                                           app->p.max_entries, d_status);
+    app->launches += 1;
+    RK_CUDA(cudaGetLastError());
+  }
+  int h_status = 0;
+  RK_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaFreeAsync(d_status, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  if (h_status == RK_ERR_SLOT_OVERFLOW)
+    return set_error(RK_ERR_SLOT_OVERFLOW, "preprocessed item exceeds slot capacity of %d entries", app->p.max_entries);
+  if (h_status == RK_ERR_MALFORMED) return set_error(RK_ERR_MALFORMED, "parsed item has no k-mers");
+  return RK_OK;
+}
+
+rk_status cv_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
+                     uint8_t* d_flags, cudaStream_t s) {
+  cv_compare_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const uint8_t*>(d_slots), slot_stride,
+                                                       app->p.max_entries, d_out, d_flags, threshold_or_nan(app));
+  app->launches += 1;
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+}  // namespace rk

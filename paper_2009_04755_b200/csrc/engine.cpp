@@ -1,0 +1,392 @@
+// All-pairs engine: quadtree leaves (scheduler.py:20-117) over a device slot
+// tier (slotcache.py:139-282) fed by the load pipeline (engine.py:436-508).
+//
+// The driver is one host thread per GPU that enqueues everything on CUDA
+// streams, so the tier's WRITE state never blocks: a slot is published as
+// soon as its preprocess is enqueued, and stream order makes the data visible
+// to every later compare.  Eviction may overwrite a slot only after every
+// compare that reads it has been enqueued (pending pairs are flushed first),
+// which is the reference's lease rule (engine.py:530-534) in stream order.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.h"
+
+namespace rk {
+
+rk_status compare_pairs(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* h_pairs, int n_pairs,
+                        double* d_out, uint8_t* d_flags, cudaStream_t s);
+int batch_limit(const rk_app* app);
+
+// ---------------------------------------------------------------------------
+// Quadtree (Region.split / iter_leaves, scheduler.py:33-86)
+int64_t region_pairs(int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  int64_t full_rows = std::max<int64_t>(0, std::min(r1, c0) - r0);
+  int64_t total = full_rows * (c1 - c0);
+  const int64_t a = std::max(r0, c0);
+  const int64_t b = std::min(r1, c1 - 1);
+  if (b > a) total += (c1 - 1 - a + c1 - b) * (b - a) / 2;
+  return total;
+}
+
+static void leaves_rec(int32_t r0, int32_t r1, int32_t c0, int32_t c1, int leaf, std::vector<Leaf>& out) {
+  if (region_pairs(r0, r1, c0, c1) == 0) return;
+  if (r1 - r0 <= leaf && c1 - c0 <= leaf) {
+    out.push_back(Leaf{r0, r1, c0, c1});
+    return;
+  }
+  const int32_t rm = (r0 + r1) / 2, cm = (c0 + c1) / 2;
+  leaves_rec(r0, rm, c0, cm, leaf, out);
+  leaves_rec(r0, rm, cm, c1, leaf, out);
+  leaves_rec(rm, r1, c0, cm, leaf, out);
+  leaves_rec(rm, r1, cm, c1, leaf, out);
+}
+
+std::vector<Leaf> quadtree_leaves(int32_t n, int leaf_block) {
+  std::vector<Leaf> out;
+  if (n >= 2) leaves_rec(0, n, 0, n, leaf_block, out);
+  return out;
+}
+
+// Contiguous DFS blocks of leaves balanced by pair count (locality per rank).
+std::vector<Leaf> rank_share(const std::vector<Leaf>& leaves, int rank, int world) {
+  if (world <= 1) return leaves;
+  int64_t total = 0;
+  for (const Leaf& l : leaves) total += region_pairs(l.r0, l.r1, l.c0, l.c1);
+  std::vector<Leaf> mine;
+  int64_t prefix = 0;
+  for (const Leaf& l : leaves) {
+    const int64_t pc = region_pairs(l.r0, l.r1, l.c0, l.c1);
+    // owner = rank whose share contains the leaf's midpoint
+    const int64_t mid = prefix + pc / 2;
+    const int owner = (int)std::min<int64_t>(world - 1, (mid * world) / std::max<int64_t>(total, 1));
+    if (owner == rank) mine.push_back(l);
+    prefix += pc;
+  }
+  return mine;
+}
+
+// ---------------------------------------------------------------------------
+// Slot tier (CacheTier restated, slotcache.py:139-282)
+SlotTier::SlotTier(int cap) : capacity(cap) {
+  key.assign(cap, -1);
+  state.assign(cap, kEmpty);
+  readers.assign(cap, 0);
+  stamp.assign(cap, 0);
+  for (int s = cap - 1; s >= 0; --s) free_list.push_back(s);  // slot 0 handed out first (slotcache.py:150)
+}
+
+int SlotTier::find(int32_t k) const {
+  auto it = index.find(k);
+  return it == index.end() ? -1 : it->second;
+}
+
+TierResult SlotTier::acquire(int32_t k) {
+  const int s = find(k);
+  if (s >= 0) {
+    if (state[s] == kRead) {
+      ++hits;
+      ++readers[s];
+      stamp[s] = ++clock;
+      return TierResult{kHit, s};
+    }
+    ++waits;
+    return TierResult{kMustWait, s};
+  }
+  int slot = -1;
+  if (!free_list.empty()) {
+    slot = free_list.back();
+    free_list.pop_back();
+  } else {
+    uint64_t best = 0;
+    for (int c = 0; c < capacity; ++c) {
+      if (state[c] == kRead && readers[c] == 0 && (slot < 0 || stamp[c] < best)) {
+        slot = c;
+        best = stamp[c];
+      }
+    }
+    if (slot < 0) return TierResult{kNoEvictable, -1};
+    index.erase(key[slot]);
+    key[slot] = -1;
+    state[slot] = kEmpty;
+    ++evictions;
+    last_evicted = slot;
+  }
+  ++misses;
+  key[slot] = k;
+  state[slot] = kWrite;
+  readers[slot] = 0;
+  stamp[slot] = ++clock;
+  index[k] = slot;
+  return TierResult{kMiss, slot};
+}
+
+void SlotTier::publish(int s, bool retain) {
+  state[s] = kRead;
+  readers[s] = retain ? 1 : 0;
+}
+
+void SlotTier::abort(int s) {
+  index.erase(key[s]);
+  key[s] = -1;
+  state[s] = kEmpty;
+  free_list.push_back(s);
+}
+
+void SlotTier::release(int s) {
+  --readers[s];
+  stamp[s] = ++clock;
+}
+
+}  // namespace rk
+
+struct rk_engine {
+  rk_app_params app_params{};
+  rk_engine_params p{};
+  int device = 0;
+  rk_app* app = nullptr;
+  cudaStream_t stream = nullptr;
+  void* arena = nullptr;
+  size_t slot_stride = 0;
+  void* staging = nullptr;
+  int staging_items = 0;
+  rk::SlotTier* tier = nullptr;
+  rk_engine_stats stats{};
+  // sampled kernel timing of the compare batches
+  int profile_every = 0;
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+};
+
+using namespace rk;
+
+namespace {
+
+struct LoadReq {
+  int32_t key;
+  int32_t slot;
+};
+
+rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, uint8_t* d_flags) {
+  if (pend.empty()) return RK_OK;
+  const int lim = batch_limit(e->app);
+  for (size_t base = 0; base < pend.size(); base += lim) {
+    const int m = (int)std::min<size_t>(lim, pend.size() - base);
+    const bool timed = e->profile_every > 0 && (e->stats.tiles % e->profile_every) == 0 &&
+                       e->ev_used + 2 <= (int)e->ev.size();
+    if (timed) RK_CUDA(cudaEventRecord(e->ev[e->ev_used], e->stream));
+    RK_TRY(compare_pairs(e->app, e->arena, e->slot_stride, pend.data() + base, m, d_out, d_flags, e->stream));
+    if (timed) {
+      RK_CUDA(cudaEventRecord(e->ev[e->ev_used + 1], e->stream));
+      e->ev_used += 2;
+    }
+    e->stats.pairs_done += m;
+    e->stats.tiles += 1;
+  }
+  pend.clear();
+  return RK_OK;
+}
+
+rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_parsed, const void* d_parsed,
+                      size_t parsed_stride) {
+  if (loads.empty()) return RK_OK;
+  const size_t pbytes = e->app->parsed_bytes;
+  for (size_t base = 0; base < loads.size(); base += e->staging_items) {
+    const int m = (int)std::min<size_t>(e->staging_items, loads.size() - base);
+    std::vector<int32_t> slots(m);
+    for (int k = 0; k < m; ++k) slots[k] = loads[base + k].slot;
+    if (h_parsed) {
+      for (int k = 0; k < m; ++k) {
+        const char* src = static_cast<const char*>(h_parsed) + (size_t)loads[base + k].key * parsed_stride;
+        RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->staging) + (size_t)k * pbytes, src, pbytes,
+                                cudaMemcpyHostToDevice, e->stream));
+        e->stats.h2d_bytes += (int64_t)pbytes;
+      }
+      RK_TRY(rk_preprocess(e->app, e->staging, pbytes, m, e->arena, e->slot_stride, slots.data(), e->stream));
+    } else {
+      // device-resident parsed items: preprocess runs of consecutive keys in place
+      int k = 0;
+      while (k < m) {
+        int run = 1;
+        while (k + run < m && loads[base + k + run].key == loads[base + k].key + run) ++run;
+        const char* src = static_cast<const char*>(d_parsed) + (size_t)loads[base + k].key * parsed_stride;
+        RK_TRY(rk_preprocess(e->app, src, parsed_stride, run, e->arena, e->slot_stride, slots.data() + k, e->stream));
+        k += run;
+      }
+    }
+    e->stats.loads += m;
+  }
+  for (const LoadReq& l : loads) e->tier->publish(l.slot, true);  // retained lease (slotcache.py:188-213)
+  loads.clear();
+  return RK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params, int device,
+                           rk_engine** out) {
+  if (!app_params || !params || !out) return set_error(RK_ERR_VALUE, "null argument");
+  *out = nullptr;
+  if (params->leaf_block < 1) return set_error(RK_ERR_VALUE, "leaf_block must be >= 1");
+  if (params->world < 1 || params->rank < 0 || params->rank >= params->world)
+    return set_error(RK_ERR_VALUE, "bad rank/world %d/%d", params->rank, params->world);
+  if (params->device_slots < 2) return set_error(RK_ERR_VALUE, "device tiers need >= 2 slots to hold a pair");
+  RK_CUDA(cudaSetDevice(device));
+  rk_engine* e = new rk_engine();
+  e->app_params = *app_params;
+  e->p = *params;
+  e->device = device;
+  rk_status st = rk_app_create(app_params, device, &e->app);
+  if (st != RK_OK) {
+    delete e;
+    return st;
+  }
+  auto fail = [&](rk_status s) {
+    rk_engine_destroy(e);
+    return s;
+  };
+  e->slot_stride = (e->app->slot_bytes + 255) / 256 * 256;
+  cudaError_t ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaStreamCreate"));
+  ce = cudaMalloc(&e->arena, e->slot_stride * (size_t)params->device_slots);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(slot arena)"));
+  e->staging_items = std::max(1, batch_limit(e->app));
+  if (e->app->p.kind == RK_APP_PCE) e->staging_items = e->app->pce.batch;
+  ce = cudaMalloc(&e->staging, std::max<size_t>(e->app->parsed_bytes, 16) * e->staging_items);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(staging)"));
+  e->tier = new SlotTier(params->device_slots);
+  *out = e;
+  return RK_OK;
+}
+
+void rk_engine_destroy(rk_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  cudaFree(e->arena);
+  cudaFree(e->staging);
+  delete e->tier;
+  rk_app_destroy(e->app);
+  delete e;
+}
+
+rk_status rk_engine_set_profiling(rk_engine* e, int every, int max_samples) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  RK_CUDA(cudaSetDevice(e->device));
+  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  e->ev.clear();
+  e->profile_every = every;
+  if (every > 0) {
+    e->ev.resize((size_t)2 * std::max(1, max_samples));
+    for (auto& ev : e->ev) RK_CUDA(cudaEventCreate(&ev));
+  }
+  e->ev_used = 0;
+  return RK_OK;
+}
+
+rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride, double* d_out,
+                        uint8_t* d_flags) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  if (!h_parsed && !d_parsed && e->app->p.kind != RK_APP_SYNTHETIC)
+    return set_error(RK_ERR_VALUE, "need host or device parsed items");
+  RK_CUDA(cudaSetDevice(e->device));
+  const int32_t n = e->app->p.n;
+  e->ev_used = 0;
+  // every run starts from a cold tier: parsed inputs may differ between runs
+  {
+    const int64_t h = e->tier->hits, m = e->tier->misses, ev = e->tier->evictions;
+    *e->tier = SlotTier(e->tier->capacity);
+    e->tier->hits = h;
+    e->tier->misses = m;
+    e->tier->evictions = ev;
+  }
+  const int64_t launches0 = e->app->launches;
+  const std::vector<Leaf> leaves = rank_share(quadtree_leaves(n, e->p.leaf_block), e->p.rank, e->p.world);
+  std::vector<rk_pair> pend;
+  std::vector<LoadReq> loads;
+  std::vector<int32_t> keys;
+  std::vector<int32_t> pinned;
+  const int lim = batch_limit(e->app);
+  for (const Leaf& l : leaves) {
+    if (e->app->p.kind == RK_APP_SYNTHETIC) {
+      // no item state: the hash needs only the keys (apps.py:201-208)
+      RK_TRY(rk_compare_tile(e->app, nullptr, 0, l.r0, l.r1, l.c0, l.c1, nullptr, d_out, d_flags, e->stream));
+      e->stats.pairs_done += region_pairs(l.r0, l.r1, l.c0, l.c1);
+      e->stats.tiles += 1;
+      continue;
+    }
+    // ascending key acquisition over the leaf's items (engine.py:510-516)
+    keys.clear();
+    for (int32_t k = l.r0; k < l.r1; ++k) keys.push_back(k);
+    for (int32_t k = l.c0; k < l.c1; ++k) keys.push_back(k);
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    pinned.clear();
+    for (int32_t k : keys) {
+      const int64_t evictions_before = e->tier->evictions;
+      TierResult r = e->tier->acquire(k);
+      if (r.kind == kNoEvictable) {
+        for (int s : pinned) e->tier->release(s);
+        for (const LoadReq& q : loads) e->tier->abort(q.slot);
+        loads.clear();
+        return set_error(RK_ERR_NO_EVICTABLE, "all %d device slots are pinned (leaf needs %zu)", e->tier->capacity,
+                         keys.size());
+      }
+      if (r.kind == kMiss) {
+        // the victim may still be read by pairs not yet launched
+        if (e->tier->evictions != evictions_before) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+        loads.push_back(LoadReq{k, r.slot});
+      }
+      pinned.push_back(r.slot);
+    }
+    RK_TRY(flush_loads(e, loads, h_parsed, d_parsed, parsed_stride));
+    for (int32_t i = l.r0; i < l.r1; ++i)
+      for (int32_t j = std::max(l.c0, i + 1); j < l.c1; ++j) {
+        pend.push_back(rk_pair{i, j, e->tier->find(i), e->tier->find(j)});
+        if ((int)pend.size() >= lim) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+      }
+    for (int s : pinned) e->tier->release(s);
+  }
+  RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+  RK_CUDA(cudaStreamSynchronize(e->stream));
+  e->stats.hits = e->tier->hits;
+  e->stats.misses = e->tier->misses;
+  e->stats.evictions = e->tier->evictions;
+  e->stats.kernel_launches += e->app->launches - launches0;
+  return RK_OK;
+}
+
+rk_status rk_engine_stats_get(const rk_engine* e, rk_engine_stats* out) {
+  if (!e || !out) return set_error(RK_ERR_VALUE, "null argument");
+  *out = e->stats;
+  return RK_OK;
+}
+
+rk_status rk_engine_reset_stats(rk_engine* e) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  e->stats = rk_engine_stats{};
+  return RK_OK;
+}
+
+rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* samples) {
+  if (!e || !ms_total || !samples) return set_error(RK_ERR_VALUE, "null argument");
+  double tot = 0.0;
+  for (int q = 0; q + 1 < e->ev_used; q += 2) {
+    float ms = 0.f;
+    RK_CUDA(cudaEventElapsedTime(&ms, e->ev[q], e->ev[q + 1]));
+    tot += ms;
+  }
+  *ms_total = tot;
+  *samples = e->ev_used / 2;
+  return RK_OK;
+}
+
+void* rk_engine_stream(const rk_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// Internal state shared by the librocket translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/rocket.h"
+
+namespace rk {
+
+// Thread-local last-error message; set_error returns the status for chaining.
+rk_status set_error(rk_status st, const char* fmt, ...);
+rk_status check_cuda(cudaError_t err, const char* what);
+#define RK_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return rk::check_cuda(_e, #call); \
+  } while (0)
+#define RK_TRY(call)                                   \
+  do {                                                 \
+    rk_status _s = (call);                             \
+    if (_s != RK_OK) return _s;                        \
+  } while (0)
+
+__host__ __device__ inline int64_t pair_id(int64_t n, int64_t i, int64_t j) {
+  return i * (2 * n - i - 1) / 2 + (j - i - 1);
+}
+
+// Pairs per kernel launch are passed by value in the launch parameters, so a
+// batch needs no host->device copy and is capture-safe for CUDA graphs.
+constexpr int kMaxBatch = 64;
+struct PairBatch {
+  int32_t npairs;
+  int32_t slot_a[kMaxBatch];
+  int32_t slot_b[kMaxBatch];
+  int32_t key_i[kMaxBatch];
+  int32_t key_j[kMaxBatch];
+  int64_t pid[kMaxBatch];
+};
+
+struct SlotList {
+  int32_t n;
+  int32_t idx[kMaxBatch];
+};
+
+struct PceState {
+  int R = 0;               // group width; N = R*R
+  int N = 0;               // pattern side
+  int batch = 0;           // pairs per launch
+  float2* tw = nullptr;    // [k1][n1] W_N^(n1*k1), R*R entries
+  float2* T = nullptr;     // batch * (N/2) * N: column-pass output, column-major per pair
+  float* part = nullptr;   // batch * row_ctas * 4 floats: max, idx(bits), sumsq, unused
+  unsigned* counters = nullptr;  // batch: CTAs finished per pair
+  float2* U = nullptr;     // batch * (N/2) * N: preprocess row-pass output
+  float* mean_part = nullptr;    // batch * 64 partial sums
+};
+
+struct CvState {};
+struct NccState {
+  float* norms = nullptr;
+};
+struct GmmState {};
+
+}  // namespace rk
+
+struct rk_app {
+  rk_app_params p{};
+  int device = 0;
+  size_t slot_bytes = 0;
+  size_t parsed_bytes = 0;
+  int64_t launches = 0;    // kernels launched through this app (for bench accounting)
+  rk::PceState pce;
+  rk::NccState ncc;
+};
+
+namespace rk {
+// Per-kind implementations (each in its own .cu).
+rk_status pce_init(rk_app* app);
+void pce_free(rk_app* app);
+rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items,
+                         void* d_slots, size_t slot_stride, const int32_t* h_slot_idx,
+                         cudaStream_t s);
+rk_status pce_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b,
+                      double* d_out, uint8_t* d_flags, cudaStream_t s);
+
+rk_status synth_compare(rk_app* app, const PairBatch& b, double* d_out, uint8_t* d_flags,
+                        cudaStream_t s);
+
+double threshold_or_nan(const rk_app* app);
+
+// Quadtree leaf [r0, r1) x [c0, c1) (Region, scheduler.py:20-71).
+struct Leaf {
+  int32_t r0, r1, c0, c1;
+};
+int64_t region_pairs(int64_t r0, int64_t r1, int64_t c0, int64_t c1);
+std::vector<Leaf> quadtree_leaves(int32_t n, int leaf_block);
+std::vector<Leaf> rank_share(const std::vector<Leaf>& leaves, int rank, int world);
+
+// Device-tier slot table: the CacheTier policy (slotcache.py:139-282) for a
+// single-threaded, stream-ordered driver.  Slot payloads live in the HBM arena.
+enum SlotState : uint8_t { kEmpty = 0, kWrite = 1, kRead = 2 };
+enum TierKind { kHit = 0, kMustWait = 1, kMiss = 2, kNoEvictable = 3 };
+struct TierResult {
+  int kind;
+  int slot;
+};
+struct SlotTier {
+  explicit SlotTier(int cap);
+  TierResult acquire(int32_t key);
+  void publish(int slot, bool retain);
+  void abort(int slot);
+  void release(int slot);
+  int find(int32_t key) const;
+  int capacity;
+  std::vector<int32_t> key;
+  std::vector<uint8_t> state;
+  std::vector<int32_t> readers;
+  std::vector<uint64_t> stamp;
+  std::vector<int> free_list;
+  std::unordered_map<int32_t, int> index;
+  uint64_t clock = 0;
+  int64_t hits = 0, misses = 0, waits = 0, evictions = 0;
+  int last_evicted = -1;
+};
+}  // namespace rk

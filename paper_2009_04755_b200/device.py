@@ -1,0 +1,135 @@
+"""Thin object wrappers over the librocket handles (rk_app, rk_engine).
+
+Device memory and streams are PyTorch plumbing: tensors are handed to the C
+ABI as raw pointers; all arithmetic happens in librocket's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class DeviceApp:
+    """One rk_app on one device: preprocess and compare entry points."""
+
+    def __init__(self, params: _lib.AppParams, device: int = 0):
+        self.params = params
+        self.device = device
+        handle = C.c_void_p()
+        check(lib.rk_app_create(C.byref(params), device, C.byref(handle)))
+        self.handle = handle
+        self.slot_bytes = int(lib.rk_app_slot_bytes(handle))
+        self.parsed_bytes = int(lib.rk_app_parsed_bytes(handle))
+        self.slot_stride = (self.slot_bytes + 255) // 256 * 256
+
+    def close(self) -> None:
+        if self.handle:
+            lib.rk_app_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alloc_slots(self, count: int) -> torch.Tensor:
+        return torch.empty(count * self.slot_stride, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def preprocess(self, parsed: torch.Tensor, parsed_stride: int, n_items: int, slots: torch.Tensor,
+                   slot_idx: Sequence[int], stream=None) -> None:
+        idx = (C.c_int32 * len(slot_idx))(*slot_idx)
+        check(lib.rk_preprocess(self.handle, _ptr(parsed), parsed_stride, n_items, _ptr(slots),
+                                self.slot_stride, idx, _stream(stream)))
+
+    def compare_pairs(self, slots: torch.Tensor, pairs: Iterable[tuple[int, int, int, int]], out: torch.Tensor,
+                      flags: Optional[torch.Tensor] = None, stream=None) -> None:
+        plist = list(pairs)
+        arr = (_lib.Pair * len(plist))(*[_lib.Pair(*p) for p in plist])
+        check(lib.rk_compare_pairs(self.handle, _ptr(slots), self.slot_stride, arr, len(plist), _ptr(out),
+                                   _ptr(flags), _stream(stream)))
+
+    def compare_tile(self, slots: Optional[torch.Tensor], r0: int, r1: int, c0: int, c1: int,
+                     slot_of_key: Sequence[int], out: torch.Tensor, flags: Optional[torch.Tensor] = None,
+                     stream=None) -> None:
+        sok = (C.c_int32 * max(1, len(slot_of_key)))(*slot_of_key)
+        check(lib.rk_compare_tile(self.handle, _ptr(slots), self.slot_stride, r0, r1, c0, c1, sok, _ptr(out),
+                                  _ptr(flags), _stream(stream)))
+
+
+def synth_prnu(h: int, w: int, first_key: int, n_items: int, cameras: int, seed: int,
+               out: torch.Tensor, stream=None) -> torch.Tensor:
+    """Deterministic PRNU-like fp32 patterns into `out` (device, n_items*h*w floats)."""
+    assert out.dtype == torch.float32 and out.is_cuda and out.numel() >= n_items * h * w
+    check(lib.rk_synth_prnu(h, w, first_key, n_items, cameras, seed & ((1 << 64) - 1), _ptr(out),
+                            _stream(stream)))
+    return out
+
+
+class DeviceEngine:
+    """rk_engine: quadtree tiles over an HBM slot tier, fed by host or device items."""
+
+    def __init__(self, params: _lib.AppParams, *, leaf_block: int = 8, device_slots: int = 0,
+                 rank: int = 0, world: int = 1, device: int = 0):
+        self.params = params
+        self.device = device
+        slots = device_slots if device_slots > 0 else max(2, params.n)
+        ep = _lib.EngineParams(leaf_block, slots, 1, rank, world)
+        handle = C.c_void_p()
+        check(lib.rk_engine_create(C.byref(params), C.byref(ep), device, C.byref(handle)))
+        self.handle = handle
+        self.engine_params = ep
+
+    def close(self) -> None:
+        if self.handle:
+            lib.rk_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, out: torch.Tensor, flags: Optional[torch.Tensor] = None, *,
+            host_items: Optional[torch.Tensor] = None, device_items: Optional[torch.Tensor] = None,
+            parsed_stride: int = 0) -> None:
+        check(lib.rk_engine_run(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride, _ptr(out),
+                                _ptr(flags)))
+
+    def stats(self) -> dict:
+        st = _lib.EngineStats()
+        check(lib.rk_engine_stats_get(self.handle, C.byref(st)))
+        return st.as_dict()
+
+    def reset_stats(self) -> None:
+        check(lib.rk_engine_reset_stats(self.handle))
+
+    def set_profiling(self, every: int, max_samples: int = 1024) -> None:
+        check(lib.rk_engine_set_profiling(self.handle, every, max_samples))
+
+    def kernel_time(self) -> tuple[float, int]:
+        ms = C.c_double()
+        cnt = C.c_int64()
+        check(lib.rk_engine_kernel_time(self.handle, C.byref(ms), C.byref(cnt)))
+        return float(ms.value), int(cnt.value)
+
+    def stream(self) -> int:
+        return int(lib.rk_engine_stream(self.handle) or 0)

@@ -1,0 +1,150 @@
+"""PCE parity: librocket's CUDA path vs the float64 numpy oracle (oracle/pce.py).
+
+Tolerance: 1e-4 relative on PCE scores (north_star; fp32 FFTs vs float64).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import pce as opce  # noqa: E402
+from oracle import scheduler as osched  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def _lib():
+    from paper_2009_04755_b200 import _lib, device
+    return _lib, device
+
+
+def make_items(n, side, cameras=2, seed=11, first_key=0):
+    _, device = _lib()
+    buf = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
+    device.synth_prnu(side, side, first_key, n, cameras, seed, buf)
+    torch.cuda.synchronize()
+    return buf
+
+
+def unpack_slot(slot_bytes: np.ndarray, n: int) -> np.ndarray:
+    """Device slot layout -> numpy rfft2 layout (n x (n/2+1))."""
+    z = slot_bytes.view(np.complex64).reshape(n // 2, n).astype(np.complex128)  # [col][row]
+    s = np.zeros((n, n // 2 + 1), dtype=np.complex128)
+    s[:, 1:n // 2] = z[1:].T
+    p = z[0]
+    pr = np.conj(p[(-np.arange(n)) % n])
+    s[:, 0] = 0.5 * (p + pr)
+    s[:, n // 2] = (p - pr) / 2j
+    return s
+
+
+@pytest.mark.parametrize("side", [256, 1024])
+def test_preprocess_spectrum_layout(side):
+    _l, device = _lib()
+    n = 3
+    items = make_items(n, side)
+    app = device.DeviceApp(_l.app_params(_l.APP_PCE, n, height=side, width=side))
+    slots = app.alloc_slots(n)
+    app.preprocess(items, side * side * 4, n, slots, [2, 0, 1])
+    torch.cuda.synchronize()
+    host = items.cpu().numpy().reshape(n, side, side)
+    raw = slots.cpu().numpy()
+    for k, slot in zip(range(n), [2, 0, 1]):
+        got = unpack_slot(raw[slot * app.slot_stride: slot * app.slot_stride + app.slot_bytes], side)
+        want = opce.preprocess(host[k]) / side
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err < 1e-5, (side, k, err)   # fp32 FFT vs float64
+
+
+@pytest.mark.parametrize("side,n", [(256, 7), (1024, 4)])
+def test_allpairs_matches_oracle(side, n):
+    _l, device = _lib()
+    items = make_items(n, side, cameras=2)
+    app = device.DeviceApp(_l.app_params(_l.APP_PCE, n, height=side, width=side, threshold=60.0))
+    slots = app.alloc_slots(n)
+    app.preprocess(items, side * side * 4, n, slots, list(range(n)))
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    app.compare_tile(slots, 0, n, 0, n, list(range(n)), out, flags)
+    torch.cuda.synchronize()
+    want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
+    got = out.cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=RTOL)
+    f = flags.cpu().numpy()
+    assert set(np.unique(f)).issubset({1, 3})
+    assert np.array_equal(f == 3, got >= 60.0)
+    # same-camera pairs separate from different-camera pairs
+    for i in range(n):
+        for j in range(i + 1, n):
+            v = got[osched.pair_id(n, i, j)]
+            assert (v > 60.0) == (i % 2 == j % 2), (i, j, v)
+
+
+def test_shifted_copy_peak():
+    _l, device = _lib()
+    side = 256
+    base = make_items(1, side, cameras=1, seed=3).view(side, side)
+    shifted = torch.roll(base, shifts=(5, -9), dims=(0, 1))
+    items = torch.stack([base, shifted]).contiguous().view(-1)
+    app = device.DeviceApp(_l.app_params(_l.APP_PCE, 2, height=side, width=side))
+    slots = app.alloc_slots(2)
+    app.preprocess(items, side * side * 4, 2, slots, [0, 1])
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    app.compare_pairs(slots, [(0, 1, 0, 1)], out)
+    torch.cuda.synchronize()
+    host = items.cpu().numpy().reshape(2, side, side)
+    s0, s1 = opce.preprocess(host[0]), opce.preprocess(host[1])
+    want, _, idx = opce.pce_from_plane(opce.correlation(s0, s1, side, side))
+    assert divmod(idx, side) == ((-5) % side, 9)
+    assert out.item() == pytest.approx(want, rel=RTOL)
+    assert out.item() > 1e4
+
+
+def test_compare_rejects_unordered_pair():
+    _l, device = _lib()
+    app = device.DeviceApp(_l.app_params(_l.APP_PCE, 4, height=256, width=256))
+    slots = app.alloc_slots(2)
+    out = torch.zeros(6, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        app.compare_pairs(slots, [(2, 1, 0, 1)], out)
+    with pytest.raises(ValueError):
+        app.compare_pairs(slots, [(1, 1, 0, 1)], out)
+
+
+@pytest.mark.parametrize("device_slots,leaf", [(64, 4), (9, 3)])
+def test_engine_matches_oracle(device_slots, leaf):
+    _l, device = _lib()
+    side, n = 256, 13
+    items = make_items(n, side, cameras=3, seed=5)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=leaf,
+                              device_slots=device_slots)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    eng.run(out, device_items=items, parsed_stride=side * side * 4)
+    st = eng.stats()
+    want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=RTOL)
+    assert st["pairs_done"] == total
+    if device_slots >= n:
+        assert st["loads"] == n and st["evictions"] == 0   # R = 1 at capacity >= n
+    else:
+        assert st["loads"] > n and st["evictions"] > 0
+
+
+def test_engine_host_items_matches_device_items():
+    _l, device = _lib()
+    side, n = 256, 9
+    items = make_items(n, side, cameras=2, seed=9)
+    host = items.cpu().pin_memory()
+    total = n * (n - 1) // 2
+    outs = []
+    for kw in ({"device_items": items}, {"host_items": host}):
+        eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=4)
+        out = torch.zeros(total, dtype=torch.float64, device="cuda")
+        eng.run(out, parsed_stride=side * side * 4, **kw)
+        outs.append(out.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
