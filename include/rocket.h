@@ -167,8 +167,8 @@ rk_status rk_engine_reset_stats(rk_engine* eng);
 /* Sample CUDA-event timing of every `every`-th compare batch (0 = off), at most
  * max_samples per run, on the engine's stream. */
 rk_status rk_engine_set_profiling(rk_engine* eng, int every, int max_samples);
-/* Summed device time and count of the sampled compare batches of the last run. */
-rk_status rk_engine_kernel_time(const rk_engine* eng, double* ms_total, int64_t* samples);
+/* Summed device time, count and pair total of the sampled compare launches of the last run. */
+rk_status rk_engine_kernel_time(const rk_engine* eng, double* ms_total, int64_t* samples, int64_t* pairs);
 /* The engine's cudaStream_t (for callers that order their own work after a run). */
 void* rk_engine_stream(const rk_engine* eng);
 

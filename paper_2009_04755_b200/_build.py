@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,
                      "-I", os.path.join(HERE, "..", "include")]
+    common += os.environ.get("RK_NVCC_FLAGS", "").split()
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [nvcc] + common + ["-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]

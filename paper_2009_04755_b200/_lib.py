@@ -104,7 +104,8 @@ SIGNATURES = [
     ("rk_engine_stats_get", C.c_int, [C.c_void_p, C.POINTER(EngineStats)]),
     ("rk_engine_reset_stats", C.c_int, [C.c_void_p]),
     ("rk_engine_set_profiling", C.c_int, [C.c_void_p, C.c_int, C.c_int]),
-    ("rk_engine_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("rk_engine_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64)]),
     ("rk_engine_stream", C.c_void_p, [C.c_void_p]),
 ]
 

@@ -49,7 +49,7 @@ static rk_status check_pairs(const rk_app* app, const rk_pair* h_pairs, int n_pa
 }
 
 int batch_limit(const rk_app* app) {
-  if (app->p.kind == RK_APP_PCE) return app->pce.batch;
+  if (app->p.kind == RK_APP_PCE) return kPipeMaxPairs;
   return kMaxBatch;
 }
 
@@ -57,7 +57,6 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
                         uint8_t* d_flags, cudaStream_t s) {
   switch (app->p.kind) {
     case RK_APP_SYNTHETIC: return synth_compare(app, b, d_out, d_flags, s);
-    case RK_APP_PCE: return pce_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     case RK_APP_CV: return cv_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "compare not built for app kind %d", app->p.kind);
   }
@@ -65,6 +64,7 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
 
 rk_status compare_pairs(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* h_pairs, int n_pairs,
                         double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  if (app->p.kind == RK_APP_PCE) return pce_compare_list(app, d_slots, slot_stride, h_pairs, n_pairs, d_out, d_flags, s);
   const int lim = batch_limit(app);
   PairBatch b;
   for (int base = 0; base < n_pairs; base += lim) {

@@ -158,6 +158,7 @@ struct rk_engine {
   // sampled kernel timing of the compare batches
   int profile_every = 0;
   std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_pairs;
   int ev_used = 0;
 };
 
@@ -181,6 +182,7 @@ rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, u
     RK_TRY(compare_pairs(e->app, e->arena, e->slot_stride, pend.data() + base, m, d_out, d_flags, e->stream));
     if (timed) {
       RK_CUDA(cudaEventRecord(e->ev[e->ev_used + 1], e->stream));
+      e->ev_pairs[e->ev_used / 2] = m;
       e->ev_used += 2;
     }
     e->stats.pairs_done += m;
@@ -284,6 +286,7 @@ rk_status rk_engine_set_profiling(rk_engine* e, int every, int max_samples) {
   e->profile_every = every;
   if (every > 0) {
     e->ev.resize((size_t)2 * std::max(1, max_samples));
+    e->ev_pairs.assign((size_t)std::max(1, max_samples), 0);
     for (auto& ev : e->ev) RK_CUDA(cudaEventCreate(&ev));
   }
   e->ev_used = 0;
@@ -374,16 +377,19 @@ rk_status rk_engine_reset_stats(rk_engine* e) {
   return RK_OK;
 }
 
-rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* samples) {
-  if (!e || !ms_total || !samples) return set_error(RK_ERR_VALUE, "null argument");
+rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* samples, int64_t* pairs) {
+  if (!e || !ms_total || !samples || !pairs) return set_error(RK_ERR_VALUE, "null argument");
   double tot = 0.0;
+  int64_t np = 0;
   for (int q = 0; q + 1 < e->ev_used; q += 2) {
     float ms = 0.f;
     RK_CUDA(cudaEventElapsedTime(&ms, e->ev[q], e->ev[q + 1]));
     tot += ms;
+    np += e->ev_pairs[q / 2];
   }
   *ms_total = tot;
   *samples = e->ev_used / 2;
+  *pairs = np;
   return RK_OK;
 }
 

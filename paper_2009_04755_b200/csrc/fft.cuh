@@ -5,7 +5,8 @@
 //   lane n1 holds x[n1 + R*n2] for n2 = 0..R-1 in registers,
 //   (1) R-point DFT over n2 in registers (fully unrolled radix-2, constant twiddles),
 //   (2) twiddle by W_N^(n1*k1) from a [k1][n1] table (bank-conflict free),
-//   (3) transpose through a padded (R+1)-stride shared buffer,
+//   (3) transpose through an XOR-swizzled R x R shared buffer (conflict-free
+//       for 64-bit accesses: half-warp phases hit 16 distinct bank pairs),
 //   (4) R-point DFT over n1 in registers.
 // On exit lane k1 holds X[k1 + R*k2] in v[k2] -- the same distribution as the
 // input, so callers load/store with lane-contiguous (coalesced) addresses.
@@ -109,11 +110,12 @@ __device__ __forceinline__ void dft_regs(float2 (&v)[N]) {
 
 // Four-step N = R*R complex FFT over a group of R lanes (see file header).
 //   v     : lane's R elements, v[n2] = x[lane + R*n2] on entry, X[lane + R*k2] on exit
-//   xbuf  : this group's R*(R+1) float2 shared scratch
-//   tw    : shared [k1][n1] table of W_N^(n1*k1) (forward sign), R*R entries
+//   xbuf  : this group's R*R float2 shared scratch
+//   tw    : [k1][n1] table of W_N^(n1*k1) (forward sign), R*R entries; shared
+//           memory in the persistent kernels, global (L1-resident) elsewhere
 // All lanes of the warp must call this together (uses __syncwarp()).
 template <int R, bool INV>
-__device__ __forceinline__ void group_fft(float2 (&v)[R], float2* xbuf, const float2* tw, int lane) {
+__device__ __forceinline__ void group_fft(float2 (&v)[R], float2* xbuf, const float2* __restrict__ tw, int lane) {
   dft_regs<R, INV>(v);
 #pragma unroll
   for (int k1 = 1; k1 < R; ++k1) {
@@ -122,12 +124,130 @@ __device__ __forceinline__ void group_fft(float2 (&v)[R], float2* xbuf, const fl
     v[k1] = c_mul(v[k1], w);
   }
 #pragma unroll
-  for (int k1 = 0; k1 < R; ++k1) xbuf[lane * (R + 1) + k1] = v[k1];
+  for (int k1 = 0; k1 < R; ++k1) xbuf[lane * R + (k1 ^ lane)] = v[k1];
   __syncwarp();
 #pragma unroll
-  for (int n1 = 0; n1 < R; ++n1) v[n1] = xbuf[n1 * (R + 1) + lane];
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = xbuf[n1 * R + (lane ^ n1)];
   __syncwarp();
   dft_regs<R, INV>(v);
+}
+
+// ---- Hopper/Blackwell bulk-copy (TMA 1D) + mbarrier helpers -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_acq_rel_add(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// ---- L2 eviction-priority hints (createpolicy + .L2::cache_hint) -----------
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// read-only (non-coherent) 8-byte load with an L2 policy
+__device__ __forceinline__ float2 ldg_nc_hint(const float2* a, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ldg_hint_f4(const void* a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ldg_hint(const float2* a, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol) : "memory");
+  return v;
+}
+__device__ __forceinline__ void stg_hint_f4(float2* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_hint(float2* a, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(a), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* a) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+}
+
+// Bulk prefetch of [a, a + bytes) into L2 (one thread; bytes multiple of 16).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* a, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
+
+// ---- thread-block clusters -------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// Full cluster barrier with release/acquire semantics (orders global and shared::cluster memory).
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of `p` (this CTA's shared memory) in the shared window of CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st_f4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 dsmem_ld_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void dsmem_st_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_add_f32(uint32_t addr, float v) {
+  asm volatile("red.shared::cluster.add.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// Global -> shared bulk copy completing on `bar` (bytes multiple of 16, both ends 16-B aligned).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
 }  // namespace rk

@@ -47,16 +47,27 @@ struct SlotList {
   int32_t idx[kMaxBatch];
 };
 
+constexpr int kPipeMaxPairs = 1024;
+struct DevPair {
+  int32_t slot_a;
+  int32_t slot_b;
+  int64_t pid;
+};
+struct PceJob {
+  int32_t npairs;
+  int32_t depth;
+  DevPair pairs[kPipeMaxPairs];
+};
 struct PceState {
   int R = 0;               // group width; N = R*R
   int N = 0;               // pattern side
-  int batch = 0;           // pairs per launch
+  int batch = 0;           // items per preprocess launch
   float2* tw = nullptr;    // [k1][n1] W_N^(n1*k1), R*R entries
-  float2* T = nullptr;     // batch * (N/2) * N: column-pass output, column-major per pair
-  float* part = nullptr;   // batch * row_ctas * 4 floats: max, idx(bits), sumsq, unused
-  unsigned* counters = nullptr;  // batch: CTAs finished per pair
   float2* U = nullptr;     // batch * (N/2) * N: preprocess row-pass output
   float* mean_part = nullptr;    // batch * 64 partial sums
+  int clusters = 0;        // co-resident compare clusters (= pairs in flight)
+  float2* T = nullptr;     // clusters * (N/2) * N: column-pass output, one slot per cluster
+  PceJob* job = nullptr;   // host staging of the launch parameters
 };
 
 struct CvState {};
@@ -84,8 +95,9 @@ void pce_free(rk_app* app);
 rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items,
                          void* d_slots, size_t slot_stride, const int32_t* h_slot_idx,
                          cudaStream_t s);
-rk_status pce_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b,
-                      double* d_out, uint8_t* d_flags, cudaStream_t s);
+
+rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                           double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 rk_status synth_compare(rk_app* app, const PairBatch& b, double* d_out, uint8_t* d_flags,
                         cudaStream_t s);

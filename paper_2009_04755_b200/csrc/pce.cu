@@ -14,14 +14,25 @@
 // The oracle restating these definitions is oracle/pce.py (parity unpinned by
 // the reference, which has no PCE: SURVEY.md section 8(c)).
 //
-// Kernels per batch of pairs (all launched on one stream):
-//   K1 pce_corr_cols  : product + inverse column FFTs  -> T (column-major, per pair)
-//   K2 pce_rows_reduce: inverse row C2R FFTs (two rows per complex FFT), fused
-//                       max/argmax/energy reduction; the last CTA of each pair
-//                       recomputes the 11 peak rows and writes the PCE score.
-// T stays L2-resident between K1 and K2 when batch * 4 MiB fits in L2.
+// Compare kernel (pce_cluster): one thread-block cluster per pair in flight,
+// persistent over the job's pairs.  The 2-D inverse FFT needs one global
+// transpose; its intermediate T (4 MiB per pair at 1024^2) lives in an L2-sized
+// per-cluster slot, so only (#clusters x 4 MiB) of T is ever live.  Per pair:
+//   column phase  CTA q: product S_a*conj(S_b) + inverse column FFTs of its
+//                 N/2/CL columns -> T (row-major, staged through shared memory)
+//   cluster barrier (release/acquire: T visible, L1 invalidated)
+//   row phase     CTA q: inverse row C2R FFTs (two rows per complex FFT) of its
+//                 N/CL rows with fused max/argmax/energy; CTA partial -> CTA 0 (DSMEM)
+//   cluster barrier; every CTA combines the CL partials (same result everywhere)
+//   window        6 warps recompute the 11 rows around the peak and add their
+//                 11x11 energy into CTA 0 (DSMEM red.add)
+//   cluster barrier; CTA 0 writes the PCE score (and match flag).
+// Each warp prefetches its next unit's lines into L1 while it computes, so
+// global latency is overlapped with the FFT arithmetic.
 #include <math.h>
 #include <stdio.h>
+
+#include <algorithm>
 
 #include "fft.cuh"
 #include "internal.h"
@@ -30,39 +41,28 @@ namespace rk {
 
 namespace {
 
-constexpr int kGroups = 8;              // FFT groups (columns or row-pairs) per CTA
-constexpr int kRows = 2 * kGroups;      // rows per row-pass CTA
+constexpr int kGroups = 8;              // FFT groups (row-pairs / columns) per preprocess CTA
+constexpr int kRows = 2 * kGroups;      // rows per preprocess row-pass CTA
 constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] tile
 constexpr int kMeanParts = 64;          // CTAs per item in the mean reduction
 constexpr int kWin = 11;                // PCE exclusion neighbourhood side
 constexpr int kHalfWin = kWin / 2;
+// warps per compare CTA: 8 lane groups (one per row pair of a 16-row block); one CTA per SM
+__host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
+
+template <int R>
+struct ClusterShape;
+template <>
+struct ClusterShape<32> {
+  static constexpr int CL = 8;   // 15 co-resident clusters on B200: 60 MiB of live T
+};
+template <>
+struct ClusterShape<16> {
+  static constexpr int CL = 2;
+};
 
 __device__ __forceinline__ bool better(float v, int idx, float bv, int bidx) {
   return v > bv || (v == bv && idx < bidx);
-}
-
-template <int R>
-__device__ __forceinline__ void load_tw(float2* tw, const float2* __restrict__ tw_g, int tid, int nt) {
-  for (int i = tid; i < R * R; i += nt) tw[i] = tw_g[i];
-}
-
-// Half-spectrum row value A[k] of row `rr` of a [k][row] tile (k in [0, N)),
-// Hermitian-extended; column 0 holds (A[0], A[N/2]) packed, both real.
-template <int N>
-__device__ __forceinline__ float2 tile_row_value(const float2* tile, int ts, int k, int rr) {
-  if (k == 0) return make_float2(tile[rr].x, 0.f);
-  if (k == N / 2) return make_float2(tile[rr].y, 0.f);
-  if (k < N / 2) return tile[k * ts + rr];
-  return c_conj(tile[(N - k) * ts + rr]);
-}
-
-// Same from global memory: T is column-major, column k holds N rows.
-template <int N>
-__device__ __forceinline__ float2 global_row_value(const float2* __restrict__ Tp, int k, int row) {
-  if (k == 0) return make_float2(Tp[row].x, 0.f);
-  if (k == N / 2) return make_float2(Tp[row].y, 0.f);
-  if (k < N / 2) return Tp[(size_t)k * N + row];
-  return c_conj(Tp[(size_t)(N - k) * N + row]);
 }
 
 // ---------------------------------------------------------------------------
@@ -100,14 +100,13 @@ __global__ void __launch_bounds__(kGroups * R) pce_rows_fwd(const float* __restr
   constexpr int N = R * R;
   constexpr int NT = kGroups * R;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* tile = smem + R * R;                       // (N/2) x kTileStride
-  float2* xbufs = tile + (N / 2) * kTileStride;      // kGroups x R*(R+1)
+  float2* tile = smem;                               // (N/2) x kTileStride
+  float2* xbufs = tile + (N / 2) * kTileStride;      // kGroups x R*R
+  const float2* tw = tw_g;
   __shared__ float s_mean;
   const int tid = threadIdx.x;
   const int item = blockIdx.y;
   const int r0 = blockIdx.x * kRows;
-  load_tw<R>(tw, tw_g, tid, NT);
   if (tid == 0) {
     double s = 0.0;
     for (int i = 0; i < kMeanParts; ++i) s += (double)mean_part[item * kMeanParts + i];
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(kGroups * R) pce_rows_fwd(const float* __restr
   __syncthreads();
   const float mu = s_mean;
   const int g = tid / R, lane = tid % R;
-  float2* xbuf = xbufs + g * R * (R + 1);
+  float2* xbuf = xbufs + g * R * R;
   const int ra = r0 + 2 * g;
   const float* xa = pix + (size_t)item * stride_f + (size_t)ra * N;
   const float* xb = xa + N;
@@ -162,13 +161,11 @@ __global__ void __launch_bounds__(kGroups * R) pce_cols_fwd(const float2* __rest
                                                            const float2* __restrict__ tw_g) {
   constexpr int N = R * R;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
+  const float2* tw = tw_g;
   const int tid = threadIdx.x;
-  load_tw<R>(tw, tw_g, tid, kGroups * R);
-  __syncthreads();
   const int item = blockIdx.y;
   const int g = tid / R, lane = tid % R;
-  float2* xbuf = smem + R * R + g * R * (R + 1);
+  float2* xbuf = smem + g * R * R;
   const int col = blockIdx.x * kGroups + g;
   const float2* Uc = U + (size_t)item * (N / 2) * N + (size_t)col * N;
   float2 v[R];
@@ -182,54 +179,18 @@ __global__ void __launch_bounds__(kGroups * R) pce_cols_fwd(const float2* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Compare K1: P = S_a * conj(S_b) on one column group, inverse column FFT -> T.
-template <int R>
-__global__ void __launch_bounds__(kGroups * R) pce_corr_cols(PairBatch b, const char* __restrict__ slots,
-                                                            size_t slot_stride, float2* __restrict__ T,
-                                                            const float2* __restrict__ tw_g) {
-  constexpr int N = R * R;
-  extern __shared__ float2 smem[];
-  float2* tw = smem;
-  const int tid = threadIdx.x;
-  load_tw<R>(tw, tw_g, tid, kGroups * R);
-  __syncthreads();
-  const int p = blockIdx.y;
-  const int g = tid / R, lane = tid % R;
-  float2* xbuf = smem + R * R + g * R * (R + 1);
-  const int col = blockIdx.x * kGroups + g;
-  const float2* X = reinterpret_cast<const float2*>(slots + (size_t)b.slot_a[p] * slot_stride) + (size_t)col * N;
-  const float2* Y = reinterpret_cast<const float2*>(slots + (size_t)b.slot_b[p] * slot_stride) + (size_t)col * N;
-  float2 v[R];
-  if (col != 0) {
-#pragma unroll
-    for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(__ldg(X + lane + R * n2), __ldg(Y + lane + R * n2));
-  } else {
-    // Packed DC/Nyquist column: split each side into its two Hermitian parts,
-    // multiply separately, re-pack the (Hermitian) products.
-#pragma unroll
-    for (int n2 = 0; n2 < R; ++n2) {
-      const int m = lane + R * n2;
-      const int mm = (N - m) & (N - 1);
-      const float2 x = __ldg(X + m), xr = c_conj(__ldg(X + mm));
-      const float2 y = __ldg(Y + m), yr = c_conj(__ldg(Y + mm));
-      const float2 xa = c_scale(c_add(x, xr), 0.5f);
-      const float2 dx = c_sub(x, xr);
-      const float2 xb = make_float2(0.5f * dx.y, -0.5f * dx.x);
-      const float2 ya = c_scale(c_add(y, yr), 0.5f);
-      const float2 dy = c_sub(y, yr);
-      const float2 yb = make_float2(0.5f * dy.y, -0.5f * dy.x);
-      const float2 pa = c_mulc(xa, ya);
-      const float2 pb = c_mulc(xb, yb);
-      v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
-    }
-  }
-  group_fft<R, true>(v, xbuf, tw, lane);
-  float2* Tp = T + (size_t)p * (N / 2) * N + (size_t)col * N;
-#pragma unroll
-  for (int k2 = 0; k2 < R; ++k2) Tp[lane + R * k2] = v[k2];
+// T (the column pass output) layout per pair: row blocks of 16 rows; block rb
+// holds all N/2 columns x 16 rows, the 16 rows of a column in 128 contiguous
+// bytes with 16-byte chunks XOR-swizzled by (column & 7).  A column FFT stores
+// two 128-B segments per warp instruction; the row pass pulls one 64 KiB block
+// per CTA round with a bulk (TMA) copy and reads row pairs conflict-free.
+template <int N>
+__device__ __forceinline__ size_t t_index(int r, int c) {
+  const int rb = r >> 4, rr = r & 15;
+  const int pos = (((rr >> 1) ^ (c & 7)) << 1) | (rr & 1);
+  return ((size_t)rb * (N / 2) + c) * 16 + pos;
 }
 
-// Block-wide reductions for K2 (blockDim = kGroups * R threads).
 struct ArgMax {
   float v;
   int idx;
@@ -255,185 +216,339 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
-// Compare K2: inverse row FFTs of 16 rows of T, fused reductions; the last CTA
-// of each pair finalises the PCE score.
+// Hermitian-extended spectrum Z[k] = A[k] + i*B[k] of rows (ra, rb) of T at
+// k = lane + R*n2 (rows of N/2 complex values; column 0 packs DC + i*Nyquist).
 template <int R>
-__global__ void __launch_bounds__(kGroups * R) pce_rows_reduce(PairBatch b, const float2* __restrict__ T,
-                                                              float4* __restrict__ part,
-                                                              unsigned* __restrict__ counters,
-                                                              const float2* __restrict__ tw_g,
-                                                              double* __restrict__ out,
-                                                              uint8_t* __restrict__ flags, double threshold) {
+__device__ __forceinline__ void load_rows_z(float2 (&v)[R], const float2* __restrict__ Tp, int ra, int rb,
+                                            bool has_b, int lane, uint64_t pol) {
   constexpr int N = R * R;
-  constexpr int NT = kGroups * R;
-  constexpr int NW = NT / 32;
-  extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* tile = smem + R * R;   // (N/2) x kTileStride; later the groups' transpose buffers
-  __shared__ float s_v[NW];
-  __shared__ int s_i[NW];
-  __shared__ double s_d[NW];
-  __shared__ int s_last;
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) {
+    const int k = lane + R * n2;
+    int kk = (n2 < R / 2) ? k : N - k;
+    if (kk >= N / 2) kk = 0;   // lane 0 at k = N/2: the Nyquist value lives in column 0
+    const float2 ta = ldg_hint(Tp + t_index<N>(ra, kk), pol);
+    const float2 tb = has_b ? ldg_hint(Tp + t_index<N>(rb, kk), pol) : make_float2(0.f, 0.f);
+    float2 x = ta, c = tb;
+    if (n2 >= R / 2) {
+      x.y = -x.y;
+      c.y = -c.y;
+    }
+    if (kk == 0) {
+      x = make_float2(n2 == 0 ? ta.x : ta.y, 0.f);
+      c = make_float2(n2 == 0 ? tb.x : tb.y, 0.f);
+    }
+    v[n2] = make_float2(x.x - c.y, x.y + c.x);
+  }
+}
+
+// Same from a 16-row block staged in shared memory: row pair cr (rows 2cr, 2cr+1)
+// is one 16-byte chunk per frequency (conflict-free LDS.128 across 8 lanes).
+template <int R>
+__device__ __forceinline__ void block_rows_z(float2 (&v)[R], const float2* tile, int cr, int lane) {
+  constexpr int N = R * R;
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) {
+    const int k = lane + R * n2;
+    int kk = (n2 < R / 2) ? k : N - k;
+    if (kk >= N / 2) kk = 0;
+    const float4 q = *reinterpret_cast<const float4*>(tile + kk * 16 + 2 * (cr ^ (kk & 7)));
+    float2 a = make_float2(q.x, q.y), c = make_float2(q.z, q.w);
+    if (n2 >= R / 2) {
+      a.y = -a.y;
+      c.y = -c.y;
+    }
+    if (kk == 0) {
+      a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
+      c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
+    }
+    v[n2] = make_float2(a.x - c.y, a.y + c.x);
+  }
+}
+
+// Running (max, first index, sum of squares) over one row pair of C.
+template <int R>
+__device__ __forceinline__ void argmax_update(const float2 (&v)[R], int ra, int lane, float& m, int& idx, float& ss) {
+  constexpr int N = R * R;
+  float lm = -INFINITY;
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) {
+    ss = fmaf(v[k2].x, v[k2].x, ss);
+    ss = fmaf(v[k2].y, v[k2].y, ss);
+    lm = fmaxf(lm, fmaxf(v[k2].x, v[k2].y));
+  }
+  if (lm >= m) {
+    int li = 0x7fffffff;
+#pragma unroll
+    for (int k2 = R - 1; k2 >= 0; --k2)
+      if (v[k2].x == lm) li = ra * N + lane + R * k2;
+    if (li == 0x7fffffff) {
+#pragma unroll
+      for (int k2 = R - 1; k2 >= 0; --k2)
+        if (v[k2].y == lm) li = (ra + 1) * N + lane + R * k2;
+    }
+    if (lm > m || li < idx) {
+      m = lm;
+      idx = li;
+    }
+  }
+}
+
+// Optional phase timing (compile with -DPCE_PROBES): per (CTA, warp 0|last) and
+// probe point, the summed clock64 of each phase boundary into a debug buffer.
+#ifdef PCE_PROBES
+__device__ unsigned long long g_pce_probe[148 * 2 * 8];
+#define PCE_PROBE(k)                                                                                      \
+  do {                                                                                                    \
+    if (wl == 0 && (warp == 0 || warp == kCtaWarps - 1))                                                  \
+      atomicAdd(&g_pce_probe[(blockIdx.x * 2 + (warp != 0)) * 8 + (k)], (unsigned long long)clock64()); \
+  } while (0)
+#else
+#define PCE_PROBE(k) \
+  do {               \
+  } while (0)
+#endif
+
+template <int R, int CL>
+__global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
+    const PceJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T,
+    const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+  constexpr int N = R * R;
+  constexpr int G = 32 / R;               // lane groups per warp
+  constexpr int kCtaWarps = cta_warps(R);
+  constexpr int CR = kCtaWarps * G;       // columns per CTA round (one per lane group)
+  constexpr int NT = kCtaWarps * 32;
+  constexpr int NCOL = (N / 2) / CL;      // columns per CTA
+  constexpr int NRP = (N / 2) / CL;       // row pairs per CTA
+  constexpr int kPairsOfRows = (kWin + 1) / 2;
+  static_assert(NCOL * CL == N / 2 && NCOL % CR == 0 && NRP % 8 == 0 && CR == 8, "cluster split");
+  constexpr int kBlk = (N / 2) * 16;      // float2 per 16-row block of T
+  constexpr uint32_t kBlkBytes = kBlk * sizeof(float2);
+  constexpr int NB = NRP / 8;             // row blocks per CTA
+  extern __shared__ __align__(128) float2 smem[];
+  float2* tiles = smem;                   // 2 x 16-row blocks (bulk-copy double buffer)
+  float2* tw = smem + 2 * kBlk;           // R*R twiddles
+  float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
+  __shared__ float s_wpart[8];            // window energy per row pair, gathered in CTA 0
+  __shared__ float s_v[kCtaWarps];
+  __shared__ int s_i[kCtaWarps];
+  __shared__ float s_ss[kCtaWarps];
   __shared__ float s_peak;
   __shared__ int s_pidx;
   __shared__ double s_total;
 
   const int tid = threadIdx.x;
-  const int p = blockIdx.y;
-  const int r0 = blockIdx.x * kRows;
-  const int warp = tid >> 5;
-  load_tw<R>(tw, tw_g, tid, NT);
-  const float2* Tp = T + (size_t)p * (N / 2) * N;
-  for (int idx = tid; idx < (N / 2) * kRows; idx += NT) {
-    const int c = idx / kRows, rr = idx % kRows;
-    tile[c * kTileStride + rr] = Tp[(size_t)c * N + r0 + rr];
-  }
-  __syncthreads();
-  const int g = tid / R, lane = tid % R;
-  float2 v[R];
-#pragma unroll
-  for (int n2 = 0; n2 < R; ++n2) {
-    const int k = lane + R * n2;
-    const float2 a = tile_row_value<N>(tile, kTileStride, k, 2 * g);
-    const float2 c = tile_row_value<N>(tile, kTileStride, k, 2 * g + 1);
-    v[n2] = make_float2(a.x - c.y, a.y + c.x);
-  }
-  __syncthreads();  // tile becomes transpose scratch
-  float2* xbuf = tile + g * R * (R + 1);
-  group_fft<R, true>(v, xbuf, tw, lane);
-
-  ArgMax best{-INFINITY, 0x7fffffff};
-  float ss = 0.f;
-  const int ra = r0 + 2 * g;
-#pragma unroll
-  for (int k2 = 0; k2 < R; ++k2) {
-    const int s = lane + R * k2;
-    const float ca = v[k2].x, cb = v[k2].y;
-    ss = fmaf(ca, ca, ss);
-    ss = fmaf(cb, cb, ss);
-    const int ia = ra * N + s;
-    if (better(ca, ia, best.v, best.idx)) best = ArgMax{ca, ia};
-    const int ib = ia + N;
-    if (better(cb, ib, best.v, best.idx)) best = ArgMax{cb, ib};
-  }
-  best = warp_argmax(best);
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) {
-    s_v[warp] = best.v;
-    s_i[warp] = best.idx;
-    s_d[warp] = (double)ss;
-  }
-  __syncthreads();
+  const int warp = tid >> 5, wl = tid & 31;
+  const int g = wl / R, lane = wl % R;
+  const int grp = warp * G + g;
+  const int q = (int)cluster_ctarank();
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  float2* xbuf = xbufs + grp * R * R;
+  float2* Tp = T + (size_t)cid * (N / 2) * N;
+  for (int i = tid; i < R * R; i += NT) tw[i] = tw_g[i];
   if (tid == 0) {
-    ArgMax bb{s_v[0], s_i[0]};
-    float t = (float)s_d[0];
-    for (int w = 1; w < NW; ++w) {
-      if (better(s_v[w], s_i[w], bb.v, bb.idx)) bb = ArgMax{s_v[w], s_i[w]};
-      t += (float)s_d[w];
-    }
-    part[(size_t)p * gridDim.x + blockIdx.x] = make_float4(bb.v, __int_as_float(bb.idx), t, 0.f);
-    __threadfence();
-    s_last = (atomicAdd(&counters[p], 1u) == gridDim.x - 1);
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
   }
+  uint32_t bar_phase = 0;                 // bit b: parity of s_bar[b]
   __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+  const uint32_t part0 = dsmem_addr(&s_part[0], 0);
+  const uint32_t wpart0 = dsmem_addr(&s_wpart[0], 0);
+  // L2 residency: T (written, then read once by the row phase) is kept with
+  // evict_last; spectra and consumed T stream through with evict_first.
+  const uint64_t pol_first = l2_policy_evict_first();
+  const uint64_t pol_last = l2_policy_evict_last();
+  cluster_sync();
 
-  // ---- finalize (last CTA of pair p) ----
-  {
-    ArgMax a{-INFINITY, 0x7fffffff};
-    double t = 0.0;
-    for (int q = tid; q < (int)gridDim.x; q += NT) {
-      const float4 e = __ldcg(part + (size_t)p * gridDim.x + q);
-      const int ei = __float_as_int(e.y);
-      if (better(e.x, ei, a.v, a.idx)) a = ArgMax{e.x, ei};
-      t += (double)e.z;
+  for (int pi = cid; pi < job.npairs; pi += ncl) {
+    const DevPair pr = job.pairs[pi];
+    float2 v[R];
+    PCE_PROBE(0);
+
+    // ---------------- column phase: NCOL columns in rounds of CR ----------------
+    const float2* Xs = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_a * slot_stride);
+    const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
+#pragma unroll 1
+    for (int c0 = q * NCOL; c0 < (q + 1) * NCOL; c0 += CR) {
+      const int col = c0 + grp;
+      const float2* X = Xs + (size_t)col * N;
+      const float2* Y = Ys + (size_t)col * N;
+      if (c0 + CR < (q + 1) * NCOL) {
+        // the group's next columns land in L1 while this round computes
+        constexpr int kLines = N * sizeof(float2) / 128;
+        const char* nx = reinterpret_cast<const char*>(X + (size_t)CR * N);
+        const char* ny = reinterpret_cast<const char*>(Y + (size_t)CR * N);
+#pragma unroll
+        for (int l = lane; l < kLines; l += R) {
+          prefetch_l1(nx + 128 * l);
+          prefetch_l1(ny + 128 * l);
+        }
+      }
+      if (col != 0) {
+#pragma unroll
+        for (int n2 = 0; n2 < R; ++n2)
+          v[n2] = c_mulc(ldg_nc_hint(X + lane + R * n2, pol_first), ldg_nc_hint(Y + lane + R * n2, pol_first));
+      } else {
+        // packed DC/Nyquist column: split both sides into their Hermitian parts,
+        // multiply separately, re-pack the (Hermitian) products
+#pragma unroll
+        for (int n2 = 0; n2 < R; ++n2) {
+          const int m = lane + R * n2;
+          const int mm = (N - m) & (N - 1);
+          const float2 x = __ldg(X + m), xr = c_conj(__ldg(X + mm));
+          const float2 y = __ldg(Y + m), yr = c_conj(__ldg(Y + mm));
+          const float2 xa = c_scale(c_add(x, xr), 0.5f);
+          const float2 dx = c_sub(x, xr);
+          const float2 xb = make_float2(0.5f * dx.y, -0.5f * dx.x);
+          const float2 ya = c_scale(c_add(y, yr), 0.5f);
+          const float2 dy = c_sub(y, yr);
+          const float2 yb = make_float2(0.5f * dy.y, -0.5f * dy.x);
+          const float2 pa = c_mulc(xa, ya);
+          const float2 pb = c_mulc(xb, yb);
+          v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
+        }
+      }
+      group_fft<R, true>(v, xbuf, tw, lane);
+      // row lane + R*k2 -> 16-row block (lane>>4) + (R/16)*k2, position lane&15
+      const int rr = lane & 15;
+      const int pos = (((rr >> 1) ^ (col & 7)) << 1) | (rr & 1);
+      float2* dst = Tp + ((size_t)(lane >> 4) * (N / 2) + col) * 16 + pos;
+      constexpr size_t kStep = (size_t)(R / 16) * (N / 2) * 16;
+#pragma unroll
+      for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_last);
     }
-    a = warp_argmax(a);
-    t = warp_sum(t);
-    if ((tid & 31) == 0) {
-      s_v[warp] = a.v;
-      s_i[warp] = a.idx;
-      s_d[warp] = t;
-    }
-    __syncthreads();
+    PCE_PROBE(1);
+    cluster_sync();
+    PCE_PROBE(2);
+
+    // ---------------- row phase: NB 16-row blocks, bulk-copied, double-buffered ----------------
+    const int blk0 = q * NB;   // first 16-row block of this CTA
     if (tid == 0) {
-      ArgMax bb{s_v[0], s_i[0]};
-      double tt = s_d[0];
-      for (int w = 1; w < NW; ++w) {
-        if (better(s_v[w], s_i[w], bb.v, bb.idx)) bb = ArgMax{s_v[w], s_i[w]};
-        tt += s_d[w];
+      fence_proxy_async();     // T's generic-proxy writes (ordered by the cluster barrier) -> async proxy
+      for (int b = 0; b < 2 && b < NB; ++b) {
+        mbar_expect_tx(&s_bar[b], kBlkBytes);
+        bulk_g2s(tiles + b * kBlk, Tp + (size_t)(blk0 + b) * kBlk, kBlkBytes, &s_bar[b]);
+      }
+    }
+    float m = -INFINITY, ss = 0.f;
+    int idx = 0x7fffffff;
+#pragma unroll 1
+    for (int b = 0; b < NB; ++b) {
+      const int buf = b & 1;
+      mbar_wait(&s_bar[buf], (bar_phase >> buf) & 1u);
+      bar_phase ^= 1u << buf;
+      const int cr = grp;                     // row pair within the block (CR == 8 row pairs)
+      block_rows_z<R>(v, tiles + buf * kBlk, cr, lane);
+      __syncthreads();                        // the block is consumed: refill it
+      if (tid == 0 && b + 2 < NB) {
+        fence_proxy_async();
+        mbar_expect_tx(&s_bar[buf], kBlkBytes);
+        bulk_g2s(tiles + buf * kBlk, Tp + (size_t)(blk0 + b + 2) * kBlk, kBlkBytes, &s_bar[buf]);
+      }
+      group_fft<R, true>(v, xbuf, tw, lane);
+      argmax_update<R>(v, 2 * (8 * (blk0 + b) + cr), lane, m, idx, ss);
+    }
+    PCE_PROBE(3);
+    {
+      ArgMax best = warp_argmax(ArgMax{m, idx});
+      ss = warp_sum(ss);
+      if (wl == 0) {
+        s_v[warp] = best.v;
+        s_i[warp] = best.idx;
+        s_ss[warp] = ss;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        ArgMax bb{s_v[0], s_i[0]};
+        float t = s_ss[0];
+        for (int w = 1; w < kCtaWarps; ++w) {
+          if (better(s_v[w], s_i[w], bb.v, bb.idx)) bb = ArgMax{s_v[w], s_i[w]};
+          t += s_ss[w];
+        }
+        dsmem_st_f4(part0 + q * sizeof(float4), make_float4(bb.v, __int_as_float(bb.idx), t, 0.f));
+      }
+    }
+    cluster_sync();
+    PCE_PROBE(4);
+    if (tid == 0) {
+      ArgMax bb{-INFINITY, 0x7fffffff};
+      double tt = 0.0;
+      for (int c = 0; c < CL; ++c) {
+        const float4 e = dsmem_ld_f4(part0 + c * sizeof(float4));
+        const int ei = __float_as_int(e.y);
+        if (better(e.x, ei, bb.v, bb.idx)) bb = ArgMax{e.x, ei};
+        tt += (double)e.z;
       }
       s_peak = bb.v;
       s_pidx = bb.idx;
       s_total = tt;
     }
     __syncthreads();
-  }
-  const int pr = s_pidx / N, pc = s_pidx % N;
-  float wsum = 0.f;
-  constexpr int kPairsOfRows = (kWin + 1) / 2;  // 6 groups recompute 11 rows
-  if (g < kPairsOfRows) {
-    const int t0 = 2 * g, t1 = 2 * g + 1;
-    const bool has_b = t1 < kWin;
-    const int rowa = (pr - kHalfWin + t0 + N) & (N - 1);
-    const int rowb = (pr - kHalfWin + t1 + N) & (N - 1);
+
+    // ---------------- window: 11 rows around the peak ----------------
+    {
+      const int prow = s_pidx / N, pcol = s_pidx % N;
+      const int t = q + CL * warp;   // one row pair per warp: t = 0..5
+      if (t < kPairsOfRows) {
+        const bool has_b = (2 * t + 1) < kWin && g == 0;
+        const int rowa = (prow - kHalfWin + 2 * t + N) & (N - 1);
+        const int rowb = (prow - kHalfWin + 2 * t + 1 + N) & (N - 1);
+        load_rows_z<R>(v, Tp, rowa, rowb, has_b, lane, pol_first);
+        if (g != 0) {   // R = 16: the warp's second lane group has no row pair
 #pragma unroll
-    for (int n2 = 0; n2 < R; ++n2) {
-      const int k = lane + R * n2;
-      const float2 a = global_row_value<N>(Tp, k, rowa);
-      const float2 c = has_b ? global_row_value<N>(Tp, k, rowb) : make_float2(0.f, 0.f);
-      v[n2] = make_float2(a.x - c.y, a.y + c.x);
-    }
-    group_fft<R, true>(v, xbuf, tw, lane);
+          for (int n2 = 0; n2 < R; ++n2) v[n2] = make_float2(0.f, 0.f);
+        }
+        group_fft<R, true>(v, xbuf, tw, lane);
+        float w = 0.f;
 #pragma unroll
-    for (int k2 = 0; k2 < R; ++k2) {
-      const int s = lane + R * k2;
-      if (((s - pc + kHalfWin + N) & (N - 1)) < kWin) {
-        wsum = fmaf(v[k2].x, v[k2].x, wsum);
-        if (has_b) wsum = fmaf(v[k2].y, v[k2].y, wsum);
+        for (int k2 = 0; k2 < R; ++k2) {
+          const int s = lane + R * k2;
+          if (((s - pcol + kHalfWin + N) & (N - 1)) < kWin) {
+            w = fmaf(v[k2].x, v[k2].x, w);
+            w = fmaf(v[k2].y, v[k2].y, w);   // zero for the padding row
+          }
+        }
+        w = warp_sum(w);
+        if (wl == 0) dsmem_st_f32(wpart0 + t * sizeof(float), w);   // fixed-order sum in CTA 0
       }
     }
-  }
-  wsum = warp_sum(wsum);
-  __syncthreads();
-  if ((tid & 31) == 0) s_d[warp] = (double)wsum;
-  __syncthreads();
-  if (tid == 0) {
-    double w = 0.0;
-    for (int q = 0; q < NW; ++q) w += s_d[q];
-    const double peak = (double)s_peak;
-    const double energy = (s_total - w) / ((double)N * (double)N - (double)(kWin * kWin));
-    const double pce = peak * fabs(peak) / energy;
-    const int64_t pid = b.pid[p];
-    out[pid] = pce;
-    if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
-    counters[p] = 0u;
+    PCE_PROBE(5);
+    cluster_sync();
+    PCE_PROBE(6);
+    if (q == 0 && tid == 0) {
+      const double peak = (double)s_peak;
+      double wsum = 0.0;
+      for (int t = 0; t < kPairsOfRows; ++t) wsum += (double)s_wpart[t];
+      const double energy = (s_total - wsum) / ((double)N * (double)N - (double)(kWin * kWin));
+      const double pce = peak * fabs(peak) / energy;
+      out[pr.pid] = pce;
+      if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
+    }
   }
 }
 
 template <int R>
-size_t cols_smem() {
-  return (size_t)(R * R + kGroups * R * (R + 1)) * sizeof(float2);
-}
-template <int R>
-size_t rows_smem() {
-  constexpr int N = R * R;
-  const size_t tile = (size_t)(N / 2) * kTileStride;
-  const size_t xb = (size_t)kGroups * R * (R + 1);
-  return (size_t)(R * R + (tile > xb ? tile : xb)) * sizeof(float2);
+size_t cols_fwd_smem() {
+  return (size_t)(kGroups * R * R) * sizeof(float2);
 }
 template <int R>
 size_t rows_fwd_smem() {
   constexpr int N = R * R;
-  return (size_t)(R * R + (N / 2) * kTileStride + kGroups * R * (R + 1)) * sizeof(float2);
+  return (size_t)((N / 2) * kTileStride + kGroups * R * R) * sizeof(float2);
+}
+template <int R>
+size_t cluster_smem() {
+  constexpr int N = R * R;
+  return (size_t)(2 * (N / 2) * 16 + R * R + cta_warps(R) * (32 / R) * R * R) * sizeof(float2);
 }
 
 template <int R>
 rk_status set_attrs() {
-  RK_CUDA(cudaFuncSetAttribute(pce_corr_cols<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<R>()));
-  RK_CUDA(cudaFuncSetAttribute(pce_cols_fwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<R>()));
-  RK_CUDA(cudaFuncSetAttribute(pce_rows_reduce<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem<R>()));
+  constexpr int CL = ClusterShape<R>::CL;
+  RK_CUDA(cudaFuncSetAttribute(pce_cluster<R, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cluster_smem<R>()));
+  RK_CUDA(cudaFuncSetAttribute(pce_cols_fwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_fwd_smem<R>()));
   RK_CUDA(cudaFuncSetAttribute(pce_rows_fwd<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_fwd_smem<R>()));
   return RK_OK;
 }
@@ -451,7 +566,7 @@ rk_status preprocess_impl(rk_app* app, const float* pix, size_t stride_f, int n_
     SlotList dst;
     dst.n = m;
     for (int k = 0; k < m; ++k) dst.idx[k] = h_slot_idx[base + k];
-    pce_cols_fwd<R><<<dim3(N / 2 / kGroups, m), kGroups * R, cols_smem<R>(), s>>>(st.U, slots, slot_stride, dst, st.tw);
+    pce_cols_fwd<R><<<dim3(N / 2 / kGroups, m), kGroups * R, cols_fwd_smem<R>(), s>>>(st.U, slots, slot_stride, dst, st.tw);
     app->launches += 3;
     RK_CUDA(cudaGetLastError());
   }
@@ -459,20 +574,71 @@ rk_status preprocess_impl(rk_app* app, const float* pix, size_t stride_f, int n_
 }
 
 template <int R>
-rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const PairBatch& b, double* d_out,
+cudaLaunchConfig_t cluster_config(int grid, cudaStream_t s, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(cta_warps(R) * 32);
+  cfg.dynamicSmemBytes = cluster_smem<R>();
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ClusterShape<R>::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+template <int R>
+rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const rk_pair* pairs, int n, double* d_out,
                        uint8_t* d_flags, cudaStream_t s) {
-  constexpr int N = R * R;
+  constexpr int CL = ClusterShape<R>::CL;
   PceState& st = app->pce;
-  if (b.npairs > st.batch) return set_error(RK_ERR_VALUE, "PCE batch of %d pairs exceeds workspace (%d)", b.npairs, st.batch);
-  pce_corr_cols<R><<<dim3(N / 2 / kGroups, b.npairs), kGroups * R, cols_smem<R>(), s>>>(b, slots, slot_stride, st.T, st.tw);
-  pce_rows_reduce<R><<<dim3(N / kRows, b.npairs), kGroups * R, rows_smem<R>(), s>>>(
-      b, st.T, reinterpret_cast<float4*>(st.part), st.counters, st.tw, d_out, d_flags, threshold_or_nan(app));
-  app->launches += 2;
-  RK_CUDA(cudaGetLastError());
+  PceJob& job = *st.job;
+  job.npairs = n;
+  job.depth = 0;
+  for (int k = 0; k < n; ++k) {
+    job.pairs[k].slot_a = pairs[k].slot_a;
+    job.pairs[k].slot_b = pairs[k].slot_b;
+    job.pairs[k].pid = pair_id(app->p.n, pairs[k].i, pairs[k].j);
+  }
+  const int clusters = std::min(st.clusters, n);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
+  RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, (const float2*)st.tw, d_out,
+                             d_flags, threshold_or_nan(app)));
+  app->launches += 1;
+  return RK_OK;
+}
+
+template <int R>
+rk_status cluster_init(rk_app* app) {
+  PceState& st = app->pce;
+  constexpr int N = R * R;
+  constexpr int CL = ClusterShape<R>::CL;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = cluster_config<R>(CL * 64, nullptr, attr);
+  int clusters = 0;
+  RK_CUDA(cudaOccupancyMaxActiveClusters(&clusters, pce_cluster<R, CL>, &cfg));
+  if (clusters < 1) return set_error(RK_ERR_DEVICE, "pce_cluster: no cluster of %d CTAs fits", CL);
+  st.clusters = clusters;
+  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * (size_t)(N / 2) * N * clusters));
+  st.job = new PceJob();
   return RK_OK;
 }
 
 }  // namespace
+
+rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                           double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  const char* slots = static_cast<const char*>(d_slots);
+  for (int base = 0; base < n; base += kPipeMaxPairs) {
+    const int m = std::min(kPipeMaxPairs, n - base);
+    if (app->pce.R == 16) RK_TRY(compare_impl<16>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
+    else RK_TRY(compare_impl<32>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
+  }
+  return RK_OK;
+}
 
 rk_status pce_init(rk_app* app) {
   const int h = app->p.height, w = app->p.width;
@@ -498,25 +664,23 @@ rk_status pce_init(rk_app* app) {
     }
   RK_CUDA(cudaMalloc(&st.tw, sizeof(float2) * R * R));
   RK_CUDA(cudaMemcpy(st.tw, tw.data(), sizeof(float2) * R * R, cudaMemcpyHostToDevice));
-  const size_t per = (size_t)(N / 2) * N;
-  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * per * st.batch));
-  st.U = st.T;  // preprocess and compare never overlap on one app (one stream per app)
-  const int row_ctas = N / kRows;
-  RK_CUDA(cudaMalloc(&st.part, sizeof(float4) * (size_t)row_ctas * st.batch));
-  RK_CUDA(cudaMalloc(&st.counters, sizeof(unsigned) * 2 * st.batch));
-  RK_CUDA(cudaMemset(st.counters, 0, sizeof(unsigned) * 2 * st.batch));
+  RK_CUDA(cudaMalloc(&st.U, sizeof(float2) * (size_t)(N / 2) * N * st.batch));
   RK_CUDA(cudaMalloc(&st.mean_part, sizeof(float) * kMeanParts * st.batch));
-  if (R == 16) return set_attrs<16>();
-  return set_attrs<32>();
+  if (R == 16) {
+    RK_TRY(set_attrs<16>());
+    return cluster_init<16>(app);
+  }
+  RK_TRY(set_attrs<32>());
+  return cluster_init<32>(app);
 }
 
 void pce_free(rk_app* app) {
   PceState& st = app->pce;
   cudaFree(st.tw);
   cudaFree(st.T);
-  cudaFree(st.part);
-  cudaFree(st.counters);
+  cudaFree(st.U);
   cudaFree(st.mean_part);
+  delete st.job;
   st = PceState{};
 }
 
@@ -530,11 +694,15 @@ rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
   return preprocess_impl<32>(app, pix, stride_f, n_items, static_cast<char*>(d_slots), slot_stride, h_slot_idx, s);
 }
 
-rk_status pce_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
-                      uint8_t* d_flags, cudaStream_t s) {
-  const char* slots = static_cast<const char*>(d_slots);
-  if (app->pce.R == 16) return compare_impl<16>(app, slots, slot_stride, b, d_out, d_flags, s);
-  return compare_impl<32>(app, slots, slot_stride, b, d_out, d_flags, s);
-}
-
 }  // namespace rk
+
+#ifdef PCE_PROBES
+extern "C" int rk_debug_pce_probes(unsigned long long* out, int n, int reset) {
+  if (cudaMemcpyFromSymbol(out, rk::g_pce_probe, sizeof(unsigned long long) * n) != cudaSuccess) return 1;
+  if (reset) {
+    static unsigned long long zeros[148 * 2 * 8] = {};
+    cudaMemcpyToSymbol(rk::g_pce_probe, zeros, sizeof(zeros));
+  }
+  return 0;
+}
+#endif

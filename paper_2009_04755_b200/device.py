@@ -125,11 +125,13 @@ class DeviceEngine:
     def set_profiling(self, every: int, max_samples: int = 1024) -> None:
         check(lib.rk_engine_set_profiling(self.handle, every, max_samples))
 
-    def kernel_time(self) -> tuple[float, int]:
+    def kernel_time(self) -> tuple[float, int, int]:
+        """(summed ms, sampled launches, pairs in those launches) of the last run."""
         ms = C.c_double()
         cnt = C.c_int64()
-        check(lib.rk_engine_kernel_time(self.handle, C.byref(ms), C.byref(cnt)))
-        return float(ms.value), int(cnt.value)
+        pairs = C.c_int64()
+        check(lib.rk_engine_kernel_time(self.handle, C.byref(ms), C.byref(cnt), C.byref(pairs)))
+        return float(ms.value), int(cnt.value), int(pairs.value)
 
     def stream(self) -> int:
         return int(lib.rk_engine_stream(self.handle) or 0)
