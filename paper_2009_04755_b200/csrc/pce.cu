@@ -368,28 +368,29 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     PCE_PROBE(0);
 
     // ---------------- column phase: NCOL columns in rounds of CR ----------------
+    // X and Y column slices of a round (CR consecutive columns, contiguous in the
+    // slots) are bulk-copied into the two tile buffers; the next round's copy is
+    // issued as soon as every group has formed its product, so it lands while
+    // the FFTs run.
     const float2* Xs = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_a * slot_stride);
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
+    constexpr uint32_t kColBytes = (uint32_t)CR * N * sizeof(float2);
+    static_assert(CR * N == kBlk, "a round's column slice fills one tile buffer");
+    if (tid == 0) {
+      mbar_expect_tx(&s_bar[0], 2 * kColBytes);
+      bulk_g2s(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0]);
+      bulk_g2s(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0]);
+    }
 #pragma unroll 1
     for (int c0 = q * NCOL; c0 < (q + 1) * NCOL; c0 += CR) {
       const int col = c0 + grp;
-      const float2* X = Xs + (size_t)col * N;
-      const float2* Y = Ys + (size_t)col * N;
-      if (c0 + CR < (q + 1) * NCOL) {
-        // the group's next columns land in L1 while this round computes
-        constexpr int kLines = N * sizeof(float2) / 128;
-        const char* nx = reinterpret_cast<const char*>(X + (size_t)CR * N);
-        const char* ny = reinterpret_cast<const char*>(Y + (size_t)CR * N);
-#pragma unroll
-        for (int l = lane; l < kLines; l += R) {
-          prefetch_l1(nx + 128 * l);
-          prefetch_l1(ny + 128 * l);
-        }
-      }
+      mbar_wait(&s_bar[0], bar_phase & 1u);
+      bar_phase ^= 1u;
+      const float2* X = tiles + grp * N;
+      const float2* Y = tiles + kBlk + grp * N;
       if (col != 0) {
 #pragma unroll
-        for (int n2 = 0; n2 < R; ++n2)
-          v[n2] = c_mulc(ldg_nc_hint(X + lane + R * n2, pol_first), ldg_nc_hint(Y + lane + R * n2, pol_first));
+        for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(X[lane + R * n2], Y[lane + R * n2]);
       } else {
         // packed DC/Nyquist column: split both sides into their Hermitian parts,
         // multiply separately, re-pack the (Hermitian) products
@@ -397,8 +398,8 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
         for (int n2 = 0; n2 < R; ++n2) {
           const int m = lane + R * n2;
           const int mm = (N - m) & (N - 1);
-          const float2 x = __ldg(X + m), xr = c_conj(__ldg(X + mm));
-          const float2 y = __ldg(Y + m), yr = c_conj(__ldg(Y + mm));
+          const float2 x = X[m], xr = c_conj(X[mm]);
+          const float2 y = Y[m], yr = c_conj(Y[mm]);
           const float2 xa = c_scale(c_add(x, xr), 0.5f);
           const float2 dx = c_sub(x, xr);
           const float2 xb = make_float2(0.5f * dx.y, -0.5f * dx.x);
@@ -409,6 +410,13 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
           const float2 pb = c_mulc(xb, yb);
           v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
         }
+      }
+      __syncthreads();   // the round's slices are consumed
+      if (tid == 0 && c0 + CR < (q + 1) * NCOL) {
+        fence_proxy_async();
+        mbar_expect_tx(&s_bar[0], 2 * kColBytes);
+        bulk_g2s(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0]);
+        bulk_g2s(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0]);
       }
       group_fft<R, true>(v, xbuf, tw, lane);
       // row lane + R*k2 -> 16-row block (lane>>4) + (R/16)*k2, position lane&15
