@@ -172,6 +172,27 @@ rk_status rk_engine_kernel_time(const rk_engine* eng, double* ms_total, int64_t*
 /* The engine's cudaStream_t (for callers that order their own work after a run). */
 void* rk_engine_stream(const rk_engine* eng);
 
+/* ---------------------------------------------------------------------------
+ * Host-side runtime structures, exported for inspection and parity tests.
+ * ------------------------------------------------------------------------- */
+/* Slot tier: the CacheTier policy (slotcache.py:139-282) the engine runs on its
+ * device slot arena.  acquire -> *kind 0 = Hit (reader pinned), 1 = MustWait,
+ * 2 = Miss (slot claimed for writing, LRU victim evicted if needed);
+ * RK_ERR_NO_EVICTABLE when every slot is pinned. */
+typedef struct rk_tier rk_tier;
+rk_status rk_tier_create(int32_t capacity, rk_tier** out);
+void rk_tier_destroy(rk_tier* tier);
+rk_status rk_tier_acquire(rk_tier* tier, int32_t key, int32_t* kind, int32_t* slot);
+rk_status rk_tier_publish(rk_tier* tier, int32_t slot, int32_t retain);
+rk_status rk_tier_abort(rk_tier* tier, int32_t slot);
+rk_status rk_tier_release(rk_tier* tier, int32_t slot);
+/* out5 = {hits, misses, waits, evictions, occupancy} (snapshot_stats, slotcache.py:252-260) */
+rk_status rk_tier_stats(const rk_tier* tier, int64_t* out5);
+int32_t rk_tier_slot_key(const rk_tier* tier, int32_t slot);
+/* Depth-first quadtree leaves (iter_leaves, scheduler.py:78-86) of this rank's
+ * share; writes min(count, cap) leaves as (r0, r1, c0, c1) and returns count. */
+int64_t rk_leaves(int32_t n, int32_t leaf_block, int32_t rank, int32_t world, int32_t* out4, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

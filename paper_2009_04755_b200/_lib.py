@@ -107,6 +107,15 @@ SIGNATURES = [
     ("rk_engine_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64)]),
     ("rk_engine_stream", C.c_void_p, [C.c_void_p]),
+    ("rk_tier_create", C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rk_tier_destroy", None, [C.c_void_p]),
+    ("rk_tier_acquire", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("rk_tier_publish", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("rk_tier_abort", C.c_int, [C.c_void_p, C.c_int32]),
+    ("rk_tier_release", C.c_int, [C.c_void_p, C.c_int32]),
+    ("rk_tier_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    ("rk_tier_slot_key", C.c_int32, [C.c_void_p, C.c_int32]),
+    ("rk_leaves", C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int64]),
 ]
 
 

@@ -396,3 +396,86 @@ rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* s
 void* rk_engine_stream(const rk_engine* e) { return e ? (void*)e->stream : nullptr; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Test/inspection surface of the runtime's host-side structures.
+struct rk_tier {
+  rk::SlotTier t;
+  explicit rk_tier(int cap) : t(cap) {}
+};
+
+extern "C" {
+
+rk_status rk_tier_create(int32_t capacity, rk_tier** out) {
+  if (!out) return set_error(RK_ERR_VALUE, "null argument");
+  if (capacity < 1) return set_error(RK_ERR_VALUE, "capacity must be >= 1 slot");
+  *out = new rk_tier(capacity);
+  return RK_OK;
+}
+
+void rk_tier_destroy(rk_tier* t) { delete t; }
+
+rk_status rk_tier_acquire(rk_tier* t, int32_t key, int32_t* kind, int32_t* slot) {
+  if (!t || !kind || !slot) return set_error(RK_ERR_VALUE, "null argument");
+  const TierResult r = t->t.acquire(key);
+  if (r.kind == kNoEvictable)
+    return set_error(RK_ERR_NO_EVICTABLE, "all %d slots are pinned", t->t.capacity);
+  *kind = r.kind;
+  *slot = r.slot;
+  return RK_OK;
+}
+
+static rk_status tier_slot_ok(const rk_tier* t, int32_t slot, uint8_t state) {
+  if (!t) return set_error(RK_ERR_VALUE, "null tier");
+  if (slot < 0 || slot >= t->t.capacity) return set_error(RK_ERR_VALUE, "slot %d out of range", slot);
+  if (t->t.state[slot] != state) return set_error(RK_ERR_VALUE, "slot %d in wrong state", slot);
+  return RK_OK;
+}
+
+rk_status rk_tier_publish(rk_tier* t, int32_t slot, int32_t retain) {
+  RK_TRY(tier_slot_ok(t, slot, kWrite));
+  t->t.publish(slot, retain != 0);
+  return RK_OK;
+}
+
+rk_status rk_tier_abort(rk_tier* t, int32_t slot) {
+  RK_TRY(tier_slot_ok(t, slot, kWrite));
+  t->t.abort(slot);
+  return RK_OK;
+}
+
+rk_status rk_tier_release(rk_tier* t, int32_t slot) {
+  RK_TRY(tier_slot_ok(t, slot, kRead));
+  if (t->t.readers[slot] <= 0) return set_error(RK_ERR_VALUE, "double release of slot %d", slot);
+  t->t.release(slot);
+  return RK_OK;
+}
+
+rk_status rk_tier_stats(const rk_tier* t, int64_t* out5) {
+  if (!t || !out5) return set_error(RK_ERR_VALUE, "null argument");
+  out5[0] = t->t.hits;
+  out5[1] = t->t.misses;
+  out5[2] = t->t.waits;
+  out5[3] = t->t.evictions;
+  out5[4] = (int64_t)t->t.index.size();
+  return RK_OK;
+}
+
+int32_t rk_tier_slot_key(const rk_tier* t, int32_t slot) {
+  if (!t || slot < 0 || slot >= t->t.capacity) return -1;
+  return t->t.key[slot];
+}
+
+int64_t rk_leaves(int32_t n, int32_t leaf_block, int32_t rank, int32_t world, int32_t* out4, int64_t cap) {
+  if (leaf_block < 1 || world < 1 || rank < 0 || rank >= world) return -1;
+  const std::vector<Leaf> v = rank_share(quadtree_leaves(n, leaf_block), rank, world);
+  for (int64_t k = 0; k < (int64_t)v.size() && k < cap; ++k) {
+    out4[4 * k + 0] = v[k].r0;
+    out4[4 * k + 1] = v[k].r1;
+    out4[4 * k + 2] = v[k].c0;
+    out4[4 * k + 3] = v[k].c1;
+  }
+  return (int64_t)v.size();
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""Public all-pairs API: run every pair of an Application's items on B200s.
+
+The runtime under it is the C++ engine of librocket (csrc/engine.cpp): the
+quadtree leaves of the pair triangle (scheduler.py:20-117) are this rank's
+work; items are acquired per leaf in ascending key order through the device
+slot tier (slotcache.py:159-282), loaded on a miss from the pinned host tier
+(H2D + device preprocess, engine.py:436-508) and compared in batches by the
+app's fused kernels.  Results land in the packed upper triangle indexed by
+PairLedger.pair_id (scheduler.py:228-231).
+
+Multi-GPU: one process per GPU (torchrun).  Each rank runs a contiguous,
+pair-balanced block of the depth-first leaves (no data-path communication);
+the disjoint result triangles are combined on rank 0 with one NCCL reduce --
+the only collective, as in the reference's completion gather to node 0
+(engine.py:550-577).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import perfmodel
+from .apps import B200Application, ItemData, PairResult, Stage, match_from_flag
+from .device import DeviceEngine
+
+
+@dataclass
+class RunResult:
+    n: int
+    values: np.ndarray                 # float64 [C(n,2)] in pair_id order
+    flags: np.ndarray                  # uint8   [C(n,2)] wire-encoded match
+    stats: dict = field(default_factory=dict)
+    seconds: float = 0.0
+
+    @property
+    def pairs(self) -> int:
+        return self.n * (self.n - 1) // 2
+
+    @property
+    def r_factor(self) -> float:
+        """R = loads / n (runner.py:41)."""
+        return self.stats.get("loads", 0) / self.n if self.n else 0.0
+
+    @property
+    def device_hit_rate(self) -> float:
+        h, m = self.stats.get("hits", 0), self.stats.get("misses", 0)
+        return h / (h + m) if h + m else 0.0
+
+    def result(self, i: int, j: int) -> PairResult:
+        pid = i * (2 * self.n - i - 1) // 2 + (j - i - 1)
+        return PairResult(i, j, float(self.values[pid]), match_from_flag(int(self.flags[pid])))
+
+    def results(self) -> dict:
+        out = {}
+        pid = 0
+        for i in range(self.n):
+            for j in range(i + 1, self.n):
+                out[(i, j)] = PairResult(i, j, float(self.values[pid]), match_from_flag(int(self.flags[pid])))
+                pid += 1
+        return out
+
+    def efficiency(self, costs: perfmodel.StageCosts, p: int = 1) -> float:
+        """(T_min / p) / T with T_min from measured single-GPU stage costs (perfmodel.py:99-114)."""
+        return perfmodel.efficiency(perfmodel.t_min(self.n, costs), p, self.seconds)
+
+
+class AllPairsEngine:
+    """All pairs of ``app``'s items on one GPU (this rank's share of a multi-GPU job)."""
+
+    def __init__(self, app: B200Application, *, leaf_block: int = 16, device_slots: Optional[int] = None,
+                 rank: int = 0, world: int = 1):
+        self.app = app
+        self.rank = rank
+        self.world = world
+        torch.cuda.set_device(app.device)
+        slots = device_slots if device_slots is not None else app.n
+        self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
+                                 rank=rank, world=world, device=app.device)
+        self._out = torch.empty(app.n * (app.n - 1) // 2, dtype=torch.float64, device=f"cuda:{app.device}")
+        self._flags = torch.empty_like(self._out, dtype=torch.uint8)
+
+    def close(self) -> None:
+        self._eng.close()
+
+    def load_items(self, pin: bool = True) -> torch.Tensor:
+        """Run fetch_raw + parse for every key into one host buffer at the parsed stride."""
+        stride = self.app.parsed_bytes()
+        host = torch.empty(self.app.n * stride, dtype=torch.uint8, pin_memory=pin)
+        view = host.numpy().reshape(self.app.n, stride)
+        for key in range(self.app.n):
+            raw = ItemData(Stage.RAW_FILE, self.app.fetch_raw(self.app.path_for_key(key)))
+            view[key] = self.app.parsed_array(self.app.parse(key, raw))
+        return host
+
+    def run(self, host_items: Optional[torch.Tensor] = None, device_items: Optional[torch.Tensor] = None,
+            gather: bool = True) -> RunResult:
+        """One full all-pairs job; returns the packed triangle (on rank 0 when world > 1)."""
+        if host_items is None and device_items is None and self.app.kind != 0:
+            host_items = self.load_items()
+        self._out.zero_()
+        self._flags.zero_()
+        self._eng.reset_stats()
+        t0 = time.perf_counter()
+        self._eng.run(self._out, self._flags, host_items=host_items, device_items=device_items,
+                      parsed_stride=self.app.parsed_bytes())
+        if self.world > 1 and gather:
+            import torch.distributed as dist
+            # disjoint pair ids per rank: a sum is an exact gather
+            dist.reduce(self._out, dst=0, op=dist.ReduceOp.SUM)
+            dist.reduce(self._flags, dst=0, op=dist.ReduceOp.SUM)
+        values = self._out.cpu().numpy()
+        flags = self._flags.cpu().numpy()
+        return RunResult(self.app.n, values, flags, self._eng.stats(), time.perf_counter() - t0)
+
+
+def run_allpairs(app: B200Application, **kw) -> RunResult:
+    """Convenience wrapper: build an engine, run once, release it."""
+    eng = AllPairsEngine(app, **kw)
+    try:
+        return eng.run()
+    finally:
+        eng.close()
