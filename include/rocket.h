@@ -121,6 +121,13 @@ rk_status rk_compare_tile(rk_app* app, const void* d_slots, size_t slot_stride,
                           const int32_t* h_slot_of_key,
                           double* d_out, uint8_t* d_flags, void* stream);
 
+/* NCC all-pairs as a tcgen05 Gram GEMM (kind::tf32, 128x128 item tiles, TMEM
+ * accumulators, TMA pipeline) over a slot arena where item k lives in slot k
+ * (n_rows >= n slots).  Upper-triangle tiles t with t % world == rank are
+ * computed; results go to d_out[pair_id].  TF32 bound: |error| <= 2e-4. */
+rk_status rk_ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t rank,
+                      int32_t world, double* d_out, uint8_t* d_flags, void* stream);
+
 /* Deterministic synthetic inputs (test/bench data generators, not the hot path). */
 /* PRNU-like patterns: item k = 0.2*K[k % cameras] + N(0,1), fp32, h*w each. */
 rk_status rk_synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras,

@@ -95,6 +95,8 @@ SIGNATURES = [
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
     ("rk_compare_tile", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("rk_ncc_gram", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,
+                              C.c_void_p, C.c_void_p, C.c_void_p]),
     ("rk_synth_prnu", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
     ("rk_engine_create", C.c_int, [C.POINTER(AppParams), C.POINTER(EngineParams), C.c_int,

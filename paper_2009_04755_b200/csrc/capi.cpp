@@ -58,6 +58,7 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
   switch (app->p.kind) {
     case RK_APP_SYNTHETIC: return synth_compare(app, b, d_out, d_flags, s);
     case RK_APP_CV: return cv_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
+    case RK_APP_NCC: return ncc_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "compare not built for app kind %d", app->p.kind);
   }
 }
@@ -141,6 +142,7 @@ rk_status rk_app_create(const rk_app_params* params, int device, rk_app** out) {
       break;
     case RK_APP_PCE: st = pce_init(app); break;
     case RK_APP_CV: st = cv_init(app); break;
+    case RK_APP_NCC: st = ncc_init(app); break;
     default: st = set_error(RK_ERR_UNSUPPORTED, "app kind %d not built", params->kind);
   }
   if (st != RK_OK) {
@@ -155,6 +157,7 @@ void rk_app_destroy(rk_app* app) {
   if (!app) return;
   cudaSetDevice(app->device);
   if (app->p.kind == RK_APP_PCE) pce_free(app);
+  if (app->p.kind == RK_APP_NCC) ncc_free(app);
   delete app;
 }
 
@@ -173,6 +176,7 @@ rk_status rk_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
     case RK_APP_SYNTHETIC: return RK_OK;  // identity payload (apps.py:196-199)
     case RK_APP_PCE: return pce_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
     case RK_APP_CV: return cv_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
+    case RK_APP_NCC: return ncc_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "preprocess not built for app kind %d", app->p.kind);
   }
 }
@@ -198,6 +202,13 @@ rk_status rk_compare_tile(rk_app* app, const void* d_slots, size_t slot_stride, 
       pairs.push_back(rk_pair{i, j, h_slot_of_key[i], h_slot_of_key[j]});
   if (pairs.empty()) return RK_OK;
   return compare_pairs(app, d_slots, slot_stride, pairs.data(), (int)pairs.size(), d_out, d_flags, s);
+}
+
+rk_status rk_ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t rank, int32_t world,
+                      double* d_out, uint8_t* d_flags, void* stream) {
+  if (!app) return set_error(RK_ERR_VALUE, "null app");
+  if (app->p.kind != RK_APP_NCC) return set_error(RK_ERR_VALUE, "rk_ncc_gram needs an NCC app");
+  return ncc_gram(app, d_slots, slot_stride, n_rows, rank, world, d_out, d_flags, static_cast<cudaStream_t>(stream));
 }
 
 rk_status rk_synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras, uint64_t seed,

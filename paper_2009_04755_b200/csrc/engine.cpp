@@ -310,6 +310,35 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->tier->evictions = ev;
   }
   const int64_t launches0 = e->app->launches;
+  if (e->app->p.kind == RK_APP_NCC) {
+    // Gram path: every item resident in slot == key, then one tcgen05 GEMM over
+    // this rank's upper-triangle tiles
+    if (e->tier->capacity < n)
+      return set_error(RK_ERR_NO_EVICTABLE, "NCC Gram path needs device_slots >= n (%d < %d)", e->tier->capacity, n);
+    std::vector<LoadReq> all;
+    for (int32_t k = 0; k < n; ++k) {
+      const TierResult r = e->tier->acquire(k);
+      if (r.kind == kMiss) all.push_back(LoadReq{k, r.slot});
+    }
+    RK_TRY(flush_loads(e, all, h_parsed, d_parsed, parsed_stride));
+    for (int32_t k = 0; k < n; ++k) e->tier->release(e->tier->find(k));
+    RK_TRY(rk_ncc_gram(e->app, e->arena, e->slot_stride, e->tier->capacity, e->p.rank, e->p.world, d_out, d_flags,
+                       e->stream));
+    const int side = (n + 127) / 128;
+    int64_t mine = 0;
+    for (int ti = 0, t = 0; ti < side; ++ti)
+      for (int tj = ti; tj < side; ++tj, ++t)
+        if (t % e->p.world == e->p.rank)
+          mine += region_pairs(ti * 128, std::min(n, ti * 128 + 128), tj * 128, std::min(n, tj * 128 + 128));
+    e->stats.pairs_done += mine;
+    e->stats.tiles += 1;
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+    e->stats.hits = e->tier->hits;
+    e->stats.misses = e->tier->misses;
+    e->stats.evictions = e->tier->evictions;
+    e->stats.kernel_launches += e->app->launches - launches0;
+    return RK_OK;
+  }
   const std::vector<Leaf> leaves = rank_share(quadtree_leaves(n, e->p.leaf_block), e->p.rank, e->p.world);
   std::vector<rk_pair> pend;
   std::vector<LoadReq> loads;

@@ -1,0 +1,383 @@
+// Zero-lag normalised cross-correlation (NCC) for sm_100a.
+//
+//   preprocess   x^ = (x - mean x) / ||x - mean x||        (fp32, one slot = D floats)
+//   compare      ncc(i, j) = x^_i . x^_j                   (the forensics NCC)
+//
+// Two compare paths:
+//   * rk_ncc_gram  -- the all-pairs path: the Gram matrix X^ X^T over the slot
+//     arena as a tcgen05 tensor-core GEMM (kind::tf32, 128x128 tiles, TMEM
+//     accumulators, TMA-fed 4-stage mbarrier pipeline, warp-specialised
+//     producer / MMA issuer / epilogue).  Only upper-triangle tiles are launched;
+//     the epilogue writes pair_id-indexed results for i < j.  TF32 rounds the
+//     operands to 10 mantissa bits: |error| <= 2e-4 * ||x^_i|| ||x^_j|| = 2e-4
+//     absolute for normalised items (stated looser bound, tests/test_ncc_gpu.py).
+//   * rk_compare_pairs -- arbitrary pairs, one warp per pair, fp32 CUDA-core dot
+//     (the reference-style per-pair Application path).
+// Oracle: oracle/ncc.py (parity unpinned by the reference, which has no NCC).
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "fft.cuh"
+#include "internal.h"
+
+namespace rk {
+
+namespace {
+
+constexpr int kTile = 128;          // items per Gram tile side (UMMA M = N = 128)
+constexpr int kBK = 32;             // fp32 elements per 128-B swizzled smem row (one TMA box row)
+constexpr int kStages = 4;
+constexpr int kStageBytes = 2 * kTile * kBK * 4;   // A + B tiles: 32 KiB
+constexpr int kGramThreads = 128;   // 4 warps: TMA producer, MMA issuer, all four in the epilogue
+
+// ---------------------------------------------------------------------------
+// preprocess: per item two passes -- (sum, sum of squares) then normalise
+__global__ void __launch_bounds__(256) ncc_moments(const float* __restrict__ pix, size_t stride_f, int64_t d,
+                                                   double* __restrict__ part) {
+  const int item = blockIdx.y;
+  const float4* x = reinterpret_cast<const float4*>(pix + (size_t)item * stride_f);
+  const int64_t n4 = d / 4;
+  double s = 0.0, q = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    s += (double)v.x + (double)v.y + (double)v.z + (double)v.w;
+    q += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  __shared__ double rs[8], rq[8];
+  if ((threadIdx.x & 31) == 0) {
+    rs[threadIdx.x >> 5] = s;
+    rq[threadIdx.x >> 5] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tq = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      ts += rs[w];
+      tq += rq[w];
+    }
+    part[((size_t)item * gridDim.x + blockIdx.x) * 2 + 0] = ts;
+    part[((size_t)item * gridDim.x + blockIdx.x) * 2 + 1] = tq;
+  }
+}
+
+__global__ void __launch_bounds__(256) ncc_normalise(const float* __restrict__ pix, size_t stride_f, int64_t d,
+                                                     const double* __restrict__ part, int nparts, char* slots,
+                                                     size_t slot_stride, SlotList dst, int* __restrict__ status) {
+  const int item = blockIdx.y;
+  __shared__ float s_mu, s_inv;
+  if (threadIdx.x == 0) {
+    double s = 0.0, q = 0.0;
+    for (int k = 0; k < nparts; ++k) {
+      s += part[((size_t)item * nparts + k) * 2 + 0];
+      q += part[((size_t)item * nparts + k) * 2 + 1];
+    }
+    const double mu = s / (double)d;
+    const double var = q - (double)d * mu * mu;   // sum of squared deviations
+    s_mu = (float)mu;
+    s_inv = var > 0.0 ? (float)(1.0 / sqrt(var)) : 0.f;
+    if (!(var > 0.0) && blockIdx.x == 0) atomicMax(status, (int)RK_ERR_MALFORMED);   // constant item
+  }
+  __syncthreads();
+  const float mu = s_mu, inv = s_inv;
+  const float4* x = reinterpret_cast<const float4*>(pix + (size_t)item * stride_f);
+  float4* y = reinterpret_cast<float4*>(slots + (size_t)dst.idx[item] * slot_stride);
+  const int64_t n4 = d / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    y[i] = make_float4((v.x - mu) * inv, (v.y - mu) * inv, (v.z - mu) * inv, (v.w - mu) * inv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-pair path: one warp per pair, fp32 dot with float4 loads
+__global__ void __launch_bounds__(256) ncc_pairs_kernel(PairBatch b, const char* __restrict__ slots, size_t slot_stride,
+                                                        int64_t d, double* __restrict__ out,
+                                                        uint8_t* __restrict__ flags, double threshold) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 8 + warp;
+  if (p >= b.npairs) return;
+  const float4* x = reinterpret_cast<const float4*>(slots + (size_t)b.slot_a[p] * slot_stride);
+  const float4* y = reinterpret_cast<const float4*>(slots + (size_t)b.slot_b[p] * slot_stride);
+  float acc0 = 0.f, acc1 = 0.f;
+  const int64_t n4 = d / 4;
+  for (int64_t i = lane; i < n4; i += 32) {
+    const float4 u = __ldg(x + i), v = __ldg(y + i);
+    acc0 = fmaf(u.x, v.x, fmaf(u.y, v.y, acc0));
+    acc1 = fmaf(u.z, v.z, fmaf(u.w, v.w, acc1));
+  }
+  double acc = (double)acc0 + (double)acc1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    out[b.pid[p]] = acc;
+    if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (acc >= threshold ? 2 : 0));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 Gram kernel
+__device__ __forceinline__ uint64_t umma_smem_desc_sw128(uint32_t smem_addr) {
+  // K-major, 128-byte swizzle: rows of 128 B, 8-row (1 KiB) swizzle atoms.
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                         // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;               // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                         // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                         // layout: SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = N = 128
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
+  uint32_t u[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
+        "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
+        "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) r[k] = __uint_as_float(u[k]);
+}
+
+// One CTA per upper-triangle 128x128 tile of items (tiles dealt to ranks).
+__global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_constant__ CUtensorMap tmap, int n,
+                                                                   int64_t d, int tiles_per_side, int rank, int world,
+                                                                   double* __restrict__ out,
+                                                                   uint8_t* __restrict__ flags, double threshold) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // tile index -> (ti, tj), ti <= tj, row-major over the upper triangle
+  int t = blockIdx.x * world + rank;
+  int ti = 0;
+  while (t >= tiles_per_side - ti) {
+    t -= tiles_per_side - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int row0 = ti * kTile, col0 = tj * kTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kTile));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const int kblocks = (int)(d / kBK);
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      mbar_wait(&empty_bar[s], ph ^ 1u);
+      uint8_t* a = smem + (size_t)s * kStageBytes;
+      uint8_t* b = a + kTile * kBK * 4;
+      mbar_expect_tx(&full_bar[s], kStageBytes);
+      tma_load_2d(a, &tmap, kb * kBK, row0, &full_bar[s]);
+      tma_load_2d(b, &tmap, kb * kBK, col0, &full_bar[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread) ----
+    constexpr uint32_t idesc = idesc_tf32(kTile, kTile);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      mbar_wait(&full_bar[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a = smem_u32(smem + (size_t)s * kStageBytes);
+      const uint32_t b = a + kTile * kBK * 4;
+#pragma unroll
+      for (int k = 0; k < kBK / 8; ++k) {   // UMMA K = 8 for tf32: 32 B along the swizzled row
+        umma_tf32(tmem, umma_smem_desc_sw128(a + k * 32), umma_smem_desc_sw128(b + k * 32), idesc,
+                  (kb | k) != 0);
+      }
+      umma_commit(&empty_bar[s]);   // smem stage free once these MMAs retire
+    }
+    umma_commit(&done_bar);         // accumulator complete
+  }
+
+  // ---- epilogue: all four warps; warp w owns TMEM lanes (tile rows) 32w..32w+31 ----
+  __syncwarp();
+  mbar_wait(&done_bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int i = row0 + warp * 32 + lane;
+  const int64_t nn = n;
+#pragma unroll 1
+  for (int c = 0; c < kTile; c += 32) {
+    float r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
+    if (i < n) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int j = col0 + c + k;
+        if (j > i && j < n) {
+          const int64_t pid = (int64_t)i * (2 * nn - i - 1) / 2 + (j - i - 1);
+          out[pid] = (double)r[k];
+          if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | ((double)r[k] >= threshold ? 2 : 0));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTile));
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+rk_status get_encoder(EncodeTiledFn* fn) {
+  static EncodeTiledFn cached = nullptr;
+  if (!cached) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable from the driver");
+    cached = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  *fn = cached;
+  return RK_OK;
+}
+
+size_t gram_smem() { return (size_t)kStages * kStageBytes + 1024; }
+
+}  // namespace
+
+rk_status ncc_init(rk_app* app) {
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  if (d <= 0 || d % kBK != 0)
+    return set_error(RK_ERR_UNSUPPORTED, "NCC item size %lld must be a positive multiple of %d", (long long)d, kBK);
+  app->slot_bytes = (size_t)d * sizeof(float);
+  app->parsed_bytes = (size_t)d * sizeof(float);
+  RK_CUDA(cudaMalloc(&app->ncc.part, sizeof(double) * 2 * 64 * kMaxBatch));
+  RK_CUDA(cudaFuncSetAttribute(ncc_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem()));
+  return RK_OK;
+}
+
+void ncc_free(rk_app* app) {
+  cudaFree(app->ncc.part);
+  app->ncc.part = nullptr;
+}
+
+rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
+                         size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s) {
+  if (parsed_stride % 16 != 0 || slot_stride % 16 != 0)
+    return set_error(RK_ERR_VALUE, "NCC strides must be multiples of 16 bytes");
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  int* d_status = nullptr;
+  RK_CUDA(cudaMallocAsync(&d_status, sizeof(int), s));
+  RK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  const size_t stride_f = parsed_stride / sizeof(float);
+  constexpr int kParts = 64;
+  for (int base = 0; base < n_items; base += kMaxBatch) {
+    const int m = std::min(kMaxBatch, n_items - base);
+    const float* px = static_cast<const float*>(d_parsed) + (size_t)base * stride_f;
+    ncc_moments<<<dim3(kParts, m), 256, 0, s>>>(px, stride_f, d, app->ncc.part);
+    SlotList dst;
+    dst.n = m;
+    for (int k = 0; k < m; ++k) dst.idx[k] = h_slot_idx[base + k];
+    ncc_normalise<<<dim3(kParts, m), 256, 0, s>>>(px, stride_f, d, app->ncc.part, kParts,
+                                                 static_cast<char*>(d_slots), slot_stride, dst, d_status);
+    app->launches += 2;
+    RK_CUDA(cudaGetLastError());
+  }
+  int h_status = 0;
+  RK_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaFreeAsync(d_status, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  if (h_status == RK_ERR_MALFORMED) return set_error(RK_ERR_MALFORMED, "NCC item has zero variance");
+  return RK_OK;
+}
+
+rk_status ncc_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
+                      uint8_t* d_flags, cudaStream_t s) {
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  ncc_pairs_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const char*>(d_slots), slot_stride, d, d_out,
+                                                       d_flags, threshold_or_nan(app));
+  app->launches += 1;
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t rank, int32_t world,
+                   double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  const int n = app->p.n;
+  if (n_rows < n) return set_error(RK_ERR_VALUE, "Gram path needs every item resident: %d slots < n = %d", n_rows, n);
+  if (slot_stride % 16 != 0) return set_error(RK_ERR_VALUE, "slot stride must be a multiple of 16 bytes");
+  if (world < 1 || rank < 0 || rank >= world) return set_error(RK_ERR_VALUE, "bad rank/world");
+  EncodeTiledFn encode = nullptr;
+  RK_TRY(get_encoder(&encode));
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)slot_stride};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kTile};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(d_slots), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const int side = (n + kTile - 1) / kTile;
+  const int tiles = side * (side + 1) / 2;
+  const int mine = (tiles - rank + world - 1) / world;
+  if (mine <= 0) return RK_OK;
+  ncc_gram_kernel<<<mine, kGramThreads, gram_smem(), s>>>(map, n, d, side, rank, world, d_out, d_flags,
+                                                          threshold_or_nan(app));
+  app->launches += 1;
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+}  // namespace rk

@@ -1,0 +1,92 @@
+"""NCC: the tcgen05 Gram path and the per-pair path vs the float64 oracle.
+
+Stated bounds: TF32 Gram |error| <= 2e-4 (10-bit operand mantissa, normalised
+items); fp32 per-pair path |error| <= 1e-5."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import ncc as oncc  # noqa: E402
+
+
+def _mods():
+    from paper_2009_04755_b200 import _lib, device
+    return _lib, device
+
+
+def make_items(n, side, seed=3, cameras=4):
+    _, device = _mods()
+    buf = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
+    device.synth_prnu(side, side, 0, n, cameras, seed, buf)
+    return buf
+
+
+@pytest.mark.parametrize("n", [37, 200])
+def test_gram_matches_oracle(n):
+    _l, device = _mods()
+    side = 256
+    items = make_items(n, side)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_NCC, n, height=side, width=side, threshold=0.02),
+                              device_slots=n)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    got = out.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 2e-4
+    # same-camera items correlate at ~0.2^2/(1+0.2^2) = 0.038, others at ~1/sqrt(D)
+    assert np.array_equal(flags.cpu().numpy() == 3, got >= 0.02)
+    st = eng.stats()
+    assert st["pairs_done"] == total and st["loads"] == n
+
+
+def test_gram_sharded_across_ranks_covers_all_pairs():
+    _l, device = _mods()
+    n, side = 300, 128
+    items = make_items(n, side, seed=8)
+    total = n * (n - 1) // 2
+    acc = torch.zeros(total, dtype=torch.float64, device="cuda")
+    done = 0
+    for rank in range(3):
+        eng = device.DeviceEngine(_l.app_params(_l.APP_NCC, n, height=side, width=side), device_slots=n,
+                                  rank=rank, world=3)
+        out = torch.zeros(total, dtype=torch.float64, device="cuda")
+        eng.run(out, device_items=items, parsed_stride=side * side * 4)
+        acc += out
+        done += eng.stats()["pairs_done"]
+    assert done == total
+    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    assert np.max(np.abs(acc.cpu().numpy() - want)) <= 2e-4
+
+
+def test_pairs_path_and_known_answers():
+    _l, device = _mods()
+    side = 256
+    base = make_items(2, side, seed=11).view(2, side, side)
+    items = torch.stack([base[0], base[0] * 3.0 + 1.5, -base[0], base[1]]).contiguous().view(-1)
+    app = device.DeviceApp(_l.app_params(_l.APP_NCC, 4, height=side, width=side))
+    slots = app.alloc_slots(4)
+    app.preprocess(items, side * side * 4, 4, slots, [0, 1, 2, 3])
+    out = torch.zeros(6, dtype=torch.float64, device="cuda")
+    app.compare_tile(slots, 0, 4, 0, 4, [0, 1, 2, 3], out)
+    got = out.cpu().numpy()
+    want = oncc.all_pairs(items.cpu().numpy().reshape(4, side, side).astype(np.float64))
+    np.testing.assert_allclose(got, want, atol=1e-5)
+    assert got[0] == pytest.approx(1.0, abs=1e-5)       # scale/offset invariance
+    assert got[1] == pytest.approx(-1.0, abs=1e-5)      # x vs -x
+    assert abs(got[2]) < 0.05
+
+
+def test_constant_item_is_malformed():
+    _l, device = _mods()
+    from paper_2009_04755_b200.errors import MalformedInput
+    app = device.DeviceApp(_l.app_params(_l.APP_NCC, 2, height=64, width=64))
+    slots = app.alloc_slots(1)
+    flat = torch.ones(64 * 64, dtype=torch.float32, device="cuda")
+    with pytest.raises(MalformedInput):
+        app.preprocess(flat, 64 * 64 * 4, 1, slots, [0])
