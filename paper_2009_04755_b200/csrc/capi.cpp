@@ -59,6 +59,7 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
     case RK_APP_SYNTHETIC: return synth_compare(app, b, d_out, d_flags, s);
     case RK_APP_CV: return cv_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     case RK_APP_NCC: return ncc_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
+    case RK_APP_GMM: return gmm_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "compare not built for app kind %d", app->p.kind);
   }
 }
@@ -143,6 +144,7 @@ rk_status rk_app_create(const rk_app_params* params, int device, rk_app** out) {
     case RK_APP_PCE: st = pce_init(app); break;
     case RK_APP_CV: st = cv_init(app); break;
     case RK_APP_NCC: st = ncc_init(app); break;
+    case RK_APP_GMM: st = gmm_init(app); break;
     default: st = set_error(RK_ERR_UNSUPPORTED, "app kind %d not built", params->kind);
   }
   if (st != RK_OK) {
@@ -177,6 +179,7 @@ rk_status rk_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
     case RK_APP_PCE: return pce_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
     case RK_APP_CV: return cv_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
     case RK_APP_NCC: return ncc_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
+    case RK_APP_GMM: return gmm_preprocess(app, d_parsed, parsed_stride, n_items, d_slots, slot_stride, h_slot_idx, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "preprocess not built for app kind %d", app->p.kind);
   }
 }

@@ -102,6 +102,11 @@ rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride,
 rk_status synth_compare(rk_app* app, const PairBatch& b, double* d_out, uint8_t* d_flags,
                         cudaStream_t s);
 
+rk_status gmm_init(rk_app* app);
+rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
+                         size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s);
+rk_status gmm_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
+                      uint8_t* d_flags, cudaStream_t s);
 rk_status ncc_init(rk_app* app);
 void ncc_free(rk_app* app);
 rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
