@@ -69,6 +69,32 @@ class RunResult:
         return perfmodel.efficiency(perfmodel.t_min(self.n, costs), p, self.seconds)
 
 
+def rank_leaves(n: int, leaf_block: int, rank: int = 0, world: int = 1) -> list:
+    """This rank's depth-first quadtree leaves (r0, r1, c0, c1), as the C++ engine schedules them."""
+    import ctypes as C
+    from ._lib import lib
+    cnt = lib.rk_leaves(n, leaf_block, rank, world, None, 0)
+    if cnt < 0:
+        raise ValueError(f"bad leaf_block/rank/world ({leaf_block}, {rank}, {world})")
+    buf = (C.c_int32 * max(1, 4 * cnt))()
+    lib.rk_leaves(n, leaf_block, rank, world, buf, cnt)
+    return [tuple(buf[4 * k:4 * k + 4]) for k in range(cnt)]
+
+
+def gather_triangle(values: torch.Tensor, flags: Optional[torch.Tensor] = None, dst: int = 0) -> None:
+    """Combine the ranks' disjoint result triangles onto ``dst`` (NCCL on GPUs, gloo on CPU).
+
+    Every pair id is written by exactly one rank and is zero elsewhere, so a
+    sum-reduce is an exact gather -- the single collective of a multi-GPU job.
+    """
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    dist.reduce(values, dst=dst, op=dist.ReduceOp.SUM)
+    if flags is not None:
+        dist.reduce(flags, dst=dst, op=dist.ReduceOp.SUM)
+
+
 class AllPairsEngine:
     """All pairs of ``app``'s items on one GPU (this rank's share of a multi-GPU job)."""
 
@@ -109,10 +135,7 @@ class AllPairsEngine:
         self._eng.run(self._out, self._flags, host_items=host_items, device_items=device_items,
                       parsed_stride=self.app.parsed_bytes())
         if self.world > 1 and gather:
-            import torch.distributed as dist
-            # disjoint pair ids per rank: a sum is an exact gather
-            dist.reduce(self._out, dst=0, op=dist.ReduceOp.SUM)
-            dist.reduce(self._flags, dst=0, op=dist.ReduceOp.SUM)
+            gather_triangle(self._out, self._flags)
         values = self._out.cpu().numpy()
         flags = self._flags.cpu().numpy()
         return RunResult(self.app.n, values, flags, self._eng.stats(), time.perf_counter() - t0)
