@@ -1,6 +1,7 @@
 // Internal state shared by the librocket translation units (not part of the ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -117,6 +118,12 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
                    double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 double threshold_or_nan(const rk_app* app);
+
+// cuTensorMapEncodeTiled, fetched from the driver through the runtime (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+rk_status tensor_map_encoder(EncodeTiledFn* fn);
 
 // Quadtree leaf [r0, r1) x [c0, c1) (Region, scheduler.py:20-71).
 struct Leaf {

@@ -273,11 +273,11 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTile));
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+size_t gram_smem() { return (size_t)kStages * kStageBytes + 1024; }
 
-rk_status get_encoder(EncodeTiledFn* fn) {
+}  // namespace
+
+rk_status tensor_map_encoder(EncodeTiledFn* fn) {
   static EncodeTiledFn cached = nullptr;
   if (!cached) {
     void* p = nullptr;
@@ -290,10 +290,6 @@ rk_status get_encoder(EncodeTiledFn* fn) {
   *fn = cached;
   return RK_OK;
 }
-
-size_t gram_smem() { return (size_t)kStages * kStageBytes + 1024; }
-
-}  // namespace
 
 rk_status ncc_init(rk_app* app) {
   const int64_t d = (int64_t)app->p.height * app->p.width;
@@ -359,7 +355,7 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
   if (slot_stride % 16 != 0) return set_error(RK_ERR_VALUE, "slot stride must be a multiple of 16 bytes");
   if (world < 1 || rank < 0 || rank >= world) return set_error(RK_ERR_VALUE, "bad rank/world");
   EncodeTiledFn encode = nullptr;
-  RK_TRY(get_encoder(&encode));
+  RK_TRY(tensor_map_encoder(&encode));
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n_rows};
   const cuuint64_t strides[1] = {(cuuint64_t)slot_stride};
