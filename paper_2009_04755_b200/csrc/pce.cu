@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     static_assert(CR * N == kBlk, "a round's column slice fills one tile buffer");
     if (tid == 0) {
       mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-      bulk_g2s(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0]);
-      bulk_g2s(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0]);
+      bulk_g2s_hint(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_first);
+      bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_first);
     }
 #pragma unroll 1
     for (int c0 = q * NCOL; c0 < (q + 1) * NCOL; c0 += CR) {
@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       if (tid == 0 && c0 + CR < (q + 1) * NCOL) {
         fence_proxy_async();
         mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-        bulk_g2s(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0]);
-        bulk_g2s(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0]);
+        bulk_g2s_hint(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_first);
+        bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_first);
       }
       group_fft<R, true>(v, xbuf, tw, lane);
       // row lane + R*k2 -> 16-row block (lane>>4) + (R/16)*k2, position lane&15
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       fence_proxy_async();     // T's generic-proxy writes (ordered by the cluster barrier) -> async proxy
       for (int b = 0; b < 2 && b < NB; ++b) {
         mbar_expect_tx(&s_bar[b], kBlkBytes);
-        bulk_g2s(tiles + b * kBlk, Tp + (size_t)(blk0 + b) * kBlk, kBlkBytes, &s_bar[b]);
+        bulk_g2s_hint(tiles + b * kBlk, Tp + (size_t)(blk0 + b) * kBlk, kBlkBytes, &s_bar[b], pol_first);
       }
     }
     float m = -INFINITY, ss = 0.f;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       if (tid == 0 && b + 2 < NB) {
         fence_proxy_async();
         mbar_expect_tx(&s_bar[buf], kBlkBytes);
-        bulk_g2s(tiles + buf * kBlk, Tp + (size_t)(blk0 + b + 2) * kBlk, kBlkBytes, &s_bar[buf]);
+        bulk_g2s_hint(tiles + buf * kBlk, Tp + (size_t)(blk0 + b + 2) * kBlk, kBlkBytes, &s_bar[buf], pol_first);
       }
       group_fft<R, true>(v, xbuf, tw, lane);
       argmax_update<R>(v, 2 * (8 * (blk0 + b) + cr), lane, m, idx, ss);
