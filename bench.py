@@ -221,7 +221,8 @@ def main():
     items = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
     device.synth_prnu(side, side, 0, n, args.cameras, args.seed, items)
     params = _lib.app_params(_lib.APP_PCE, n, height=side, width=side, threshold=60.0)
-    eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=n, rank=rank, world=world)
+    eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=n, rank=rank, world=world,
+                              device=local_rank)
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
@@ -267,12 +268,27 @@ def main():
     e2e = None
     if not args.no_e2e:
         try:
-            host = torch.empty(n * side * side, dtype=torch.float32, pin_memory=True)
-            host.copy_(items)
+            # each rank pins only the key range its leaves touch; the engine addresses
+            # item k at base + k * stride, so the base is shifted by the range start
+            from paper_2009_04755_b200.engine import rank_leaves
+            mine = rank_leaves(n, args.leaf, rank, world)
+            lo = min(min(l[0], l[2]) for l in mine) if mine else 0
+            hi = max(max(l[1], l[3]) for l in mine) if mine else 0
+            host = torch.empty((hi - lo) * side * side, dtype=torch.float32, pin_memory=True)
+            host.copy_(items[lo * side * side: hi * side * side])
             res_host = torch.empty(pairs_total, dtype=torch.float64, pin_memory=True)
             del items
             torch.cuda.empty_cache()
-            eng.run(out, flags, host_items=host, parsed_stride=parsed_bytes)  # warm the H2D path
+
+            class _Shifted:   # a pointer view: data_ptr() of item 0 of the full array
+                def __init__(self, t, off):
+                    self.t, self.off = t, off
+
+                def data_ptr(self):
+                    return self.t.data_ptr() - self.off
+
+            host_view = _Shifted(host, lo * parsed_bytes)
+            eng.run(out, flags, host_items=host_view, parsed_stride=parsed_bytes)  # warm the H2D path
             eng.reset_stats()
             barrier()
             torch.cuda.synchronize()
@@ -282,7 +298,7 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(args.steps):
-                eng.run(out, flags, host_items=host, parsed_stride=parsed_bytes)
+                eng.run(out, flags, host_items=host_view, parsed_stride=parsed_bytes)
                 gather_triangle(out, flags)            # disjoint pair ids: exact gather to rank 0
                 res_host.copy_(out, non_blocking=True)
             e1.record()
