@@ -221,15 +221,46 @@ def main():
     items = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
     device.synth_prnu(side, side, 0, n, args.cameras, args.seed, items)
     params = _lib.app_params(_lib.APP_PCE, n, height=side, width=side, threshold=60.0)
+    # N > 1: peer-GPU tier -- each rank preprocesses its home items (k % N == rank),
+    # every other item it needs is copied from its home GPU over NVLink (CUDA IPC)
+    peer = world > 1
     eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=n, rank=rank, world=world,
-                              device=local_rank)
+                              device=local_rank, peer_tier=peer)
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
     torch.cuda.synchronize()
 
+    class _At:   # pointer view at a byte offset (the C ABI only needs data_ptr())
+        def __init__(self, t, off):
+            self.t, self.off = t, off
+
+        def data_ptr(self):
+            return self.t.data_ptr() + self.off
+
+    state = {"connected": False}
+
+    def step(host_home=None, host_all=None):
+        """One full job on this rank: [home preprocess + barrier] + all of its pairs [+ barrier]."""
+        if peer:
+            if host_home is not None:
+                eng.load_home(host_items=host_home, parsed_stride=parsed_bytes)
+            else:
+                eng.load_home(device_items=_At(items, rank * parsed_bytes), parsed_stride=world * parsed_bytes)
+            if not state["connected"]:
+                eng.connect_peers()
+                state["connected"] = True
+            barrier()
+            eng.run(out, flags, host_items=host_home, device_items=None if host_home is not None else items,
+                    parsed_stride=parsed_bytes)
+            barrier()
+        elif host_all is not None:
+            eng.run(out, flags, host_items=host_all, parsed_stride=parsed_bytes)
+        else:
+            eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+
     for _ in range(args.warmup):
-        eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+        step()
     eng.reset_stats()
     eng.set_profiling(every=3, max_samples=4096)
     clocks = ClockSampler(local_rank)
@@ -241,7 +272,7 @@ def main():
     ev0.record(estream)
     kms, ksamples, kpairs = 0.0, 0, 0
     for _ in range(args.steps):
-        eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+        step()
         a, b, c = eng.kernel_time()
         kms += a
         ksamples += b
@@ -263,32 +294,30 @@ def main():
         all_pairs = float(my_pairs)
     value = all_pairs / (ms / 1e3)
     eng.set_profiling(0)
+    # cache accounting over the whole job (runner.py:41 R = loads / n; slotcache.py:252-260 tiers)
+    ct = torch.tensor([st["loads"], st["hits"], st["misses"], st["peer_fetches"]], dtype=torch.float64,
+                      device="cuda")
+    if world > 1:
+        dist.all_reduce(ct, op=dist.ReduceOp.SUM)
+    loads_all, hits_all, misses_all, peer_all = [float(x) / max(1, args.steps) for x in ct.tolist()]
 
     # ---- e2e: pinned host patterns -> engine -> packed triangle back on host
     e2e = None
     if not args.no_e2e:
         try:
-            # each rank pins only the key range its leaves touch; the engine addresses
-            # item k at base + k * stride, so the base is shifted by the range start
-            from paper_2009_04755_b200.engine import rank_leaves
-            mine = rank_leaves(n, args.leaf, rank, world)
-            lo = min(min(l[0], l[2]) for l in mine) if mine else 0
-            hi = max(max(l[1], l[3]) for l in mine) if mine else 0
-            host = torch.empty((hi - lo) * side * side, dtype=torch.float32, pin_memory=True)
-            host.copy_(items[lo * side * side: hi * side * side])
+            if peer:
+                # a rank needs only its home items on the host (every other item comes over NVLink)
+                host = torch.empty((len(range(rank, n, world)), side * side), dtype=torch.float32, pin_memory=True)
+                host.copy_(items.view(n, side * side)[rank::world])
+                host_home, host_all = host, None
+            else:
+                host = torch.empty(n * side * side, dtype=torch.float32, pin_memory=True)
+                host.copy_(items)
+                host_home, host_all = None, host
             res_host = torch.empty(pairs_total, dtype=torch.float64, pin_memory=True)
             del items
             torch.cuda.empty_cache()
-
-            class _Shifted:   # a pointer view: data_ptr() of item 0 of the full array
-                def __init__(self, t, off):
-                    self.t, self.off = t, off
-
-                def data_ptr(self):
-                    return self.t.data_ptr() - self.off
-
-            host_view = _Shifted(host, lo * parsed_bytes)
-            eng.run(out, flags, host_items=host_view, parsed_stride=parsed_bytes)  # warm the H2D path
+            step(host_home=host_home, host_all=host_all)   # warm the H2D path
             eng.reset_stats()
             barrier()
             torch.cuda.synchronize()
@@ -298,7 +327,7 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(args.steps):
-                eng.run(out, flags, host_items=host_view, parsed_stride=parsed_bytes)
+                step(host_home=host_home, host_all=host_all)
                 gather_triangle(out, flags)            # disjoint pair ids: exact gather to rank 0
                 res_host.copy_(out, non_blocking=True)
             e1.record()
@@ -311,7 +340,8 @@ def main():
             ems = float(tt[0])
             e2e = {"value": all_pairs / (ems / 1e3), "unit": "pairs/s",
                    "h2d_bytes_per_step": int(st2["h2d_bytes"] // max(1, args.steps)),
-                   "d2h_bytes_per_step": pairs_total * 8}
+                   "d2h_bytes_per_step": pairs_total * 8,
+                   "peer_bytes_per_step": int(st2.get("peer_bytes", 0) // max(1, args.steps))}
         except RuntimeError as exc:  # e.g. pinned-memory exhaustion
             e2e = {"value": None, "unit": "pairs/s", "error": str(exc)[:200]}
 
@@ -325,12 +355,22 @@ def main():
     slot_bytes = side * side * 4
     alg_bytes_per_pair = 2 * slot_bytes          # two half-spectra per pair
     roofline = None
+    traffic = None
+    try:   # dram bytes of one pce_cluster launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "pce_cluster_traffic.json")) as fh:
+            tj = json.load(fh)
+        traffic_per_pair = (tj["dram_bytes_read_per_launch"] + tj["dram_bytes_write_per_launch"]) / tj["pairs_per_launch"]
+    except Exception:
+        traffic_per_pair = None
     if ksamples:
         per_launch_ms = kms / ksamples
         batch = kpairs / ksamples
         achieved = alg_bytes_per_pair * batch / (per_launch_ms / 1e3) / 1e9
+        if traffic_per_pair is not None:
+            traffic = traffic_per_pair * batch
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": None,
+                    "frac": achieved / hbm, "traffic": traffic,
+                    "traffic_source": "profiles/pce_cluster_traffic.json (ncu dram__bytes_read+write, per launch)",
                     "kernel": "pce_cluster (persistent 8-CTA cluster per pair: column + row pass)",
                     "pairs_per_launch": batch, "ms_per_launch": per_launch_ms,
                     "alg_bytes_per_pair": alg_bytes_per_pair, "peak_source": peaks_src,
@@ -347,9 +387,11 @@ def main():
                        "parallelism": f"pairs{world}", "l2": "inputs (16 GiB patterns + 16 GiB spectra) >> L2"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": st["kernel_launches"],
-            "cache": {"loads": st["loads"], "R": st["loads"] / n / max(1, args.steps) * world,
-                      "device_hits": st["hits"], "device_misses": st["misses"],
-                      "hit_rate": st["hits"] / max(1, st["hits"] + st["misses"])}}
+            "cache": {"R": loads_all / n, "loads_per_step": loads_all,
+                      "device_hit_rate": hits_all / max(1.0, hits_all + misses_all),
+                      "device_hits_per_step": hits_all, "device_misses_per_step": misses_all,
+                      "peer_fetches_per_step": peer_all,
+                      "peer_hit_rate": peer_all / max(1.0, misses_all) if world > 1 else None}}
     print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     eng.close()

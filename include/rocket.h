@@ -145,7 +145,8 @@ typedef struct {
   int32_t device_slots;    /* device tier capacity in slots */
   int32_t streams;         /* compare streams (each owns an rk_app workspace) */
   int32_t rank;            /* this rank's share of the leaves ... */
-  int32_t world;           /* ... out of world (leaves dealt round-robin in DFS blocks) */
+  int32_t world;           /* ... out of world (contiguous, pair-balanced DFS blocks of leaves) */
+  int32_t peer_tier;       /* world > 1: items live on their home GPU (k mod world), others fetch them over NVLink */
 } rk_engine_params;
 
 typedef struct {
@@ -158,6 +159,8 @@ typedef struct {
   int64_t h2d_bytes;
   int64_t d2h_bytes;
   int64_t kernel_launches;
+  int64_t peer_fetches;    /* items copied from a peer GPU's home region (the remote tier, distcache.py) */
+  int64_t peer_bytes;
 } rk_engine_stats;
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,
@@ -171,6 +174,23 @@ rk_status rk_engine_run(rk_engine* eng, const void* h_parsed, const void* d_pars
                         size_t parsed_stride, double* d_out, uint8_t* d_flags);
 rk_status rk_engine_stats_get(const rk_engine* eng, rk_engine_stats* out);
 rk_status rk_engine_reset_stats(rk_engine* eng);
+
+/* Peer-GPU cache tier (the point-of-contact rule owner_of(k) = k mod p,
+ * distcache.py:19-23, collapsed to one NVLink hop).  Each rank preprocesses its
+ * home items (k % world == rank) into the home region of its slot arena
+ * (item k at slot device_slots + k / world); the caller exchanges the home
+ * regions with rk_ipc_handle / rk_ipc_open and a barrier, then
+ * rk_engine_set_peer_homes; rk_engine_run copies every non-home item it needs
+ * device-to-device from its home GPU instead of reloading it from the host. */
+rk_status rk_engine_home_region(const rk_engine* eng, void** d_base, size_t* bytes);
+rk_status rk_engine_arena(const rk_engine* eng, void** d_base, size_t* slot_stride);
+/* Home item m (key = rank + m*world) is read at parsed + m*parsed_stride. */
+rk_status rk_engine_load_home(rk_engine* eng, const void* h_parsed, const void* d_parsed, size_t parsed_stride);
+rk_status rk_engine_set_peer_homes(rk_engine* eng, int32_t world, void* const* d_home_bases);
+/* CUDA IPC of a device allocation (64-byte handle) for the peer tier. */
+rk_status rk_ipc_handle(const void* d_ptr, uint8_t* out_handle64);
+rk_status rk_ipc_open(const uint8_t* handle64, int device, void** d_ptr);
+rk_status rk_ipc_close(void* d_ptr);
 /* Sample CUDA-event timing of every `every`-th compare batch (0 = off), at most
  * max_samples per run, on the engine's stream. */
 rk_status rk_engine_set_profiling(rk_engine* eng, int every, int max_samples);

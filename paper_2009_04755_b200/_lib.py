@@ -58,6 +58,7 @@ class EngineParams(C.Structure):
         ("streams", C.c_int32),
         ("rank", C.c_int32),
         ("world", C.c_int32),
+        ("peer_tier", C.c_int32),
     ]
 
 
@@ -72,6 +73,8 @@ class EngineStats(C.Structure):
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("peer_fetches", C.c_int64),
+        ("peer_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -109,6 +112,13 @@ SIGNATURES = [
     ("rk_engine_kernel_time", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64)]),
     ("rk_engine_stream", C.c_void_p, [C.c_void_p]),
+    ("rk_engine_home_region", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    ("rk_engine_arena", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    ("rk_engine_load_home", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    ("rk_engine_set_peer_homes", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rk_ipc_handle", C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    ("rk_ipc_open", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)]),
+    ("rk_ipc_close", C.c_int, [C.c_void_p]),
     ("rk_tier_create", C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     ("rk_tier_destroy", None, [C.c_void_p]),
     ("rk_tier_acquire", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),

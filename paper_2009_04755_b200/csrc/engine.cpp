@@ -155,6 +155,12 @@ struct rk_engine {
   int staging_items = 0;
   rk::SlotTier* tier = nullptr;
   rk_engine_stats stats{};
+  // peer-GPU tier (distcache.py owner_of: home(k) = k mod world): this rank's home
+  // items live at arena slots [device_slots, device_slots + home_slots), item k at
+  // device_slots + k / world; other ranks' home regions are IPC-mapped
+  int home_slots = 0;
+  std::vector<const char*> peer_home;   // per rank: base of its home region (own entry = local)
+  bool peers_ready = false;
   // sampled kernel timing of the compare batches
   int profile_every = 0;
   std::vector<cudaEvent_t> ev;
@@ -255,7 +261,9 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   e->slot_stride = (e->app->slot_bytes + 255) / 256 * 256;
   cudaError_t ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaStreamCreate"));
-  ce = cudaMalloc(&e->arena, e->slot_stride * (size_t)params->device_slots);
+  if (params->peer_tier && params->world > 1)
+    e->home_slots = (app_params->n + params->world - 1) / params->world;
+  ce = cudaMalloc(&e->arena, e->slot_stride * ((size_t)params->device_slots + e->home_slots));
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(slot arena)"));
   e->staging_items = std::max(1, batch_limit(e->app));
   if (e->app->p.kind == RK_APP_PCE) e->staging_items = e->app->pce.batch;
@@ -340,10 +348,16 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     return RK_OK;
   }
   const std::vector<Leaf> leaves = rank_share(quadtree_leaves(n, e->p.leaf_block), e->p.rank, e->p.world);
+  const bool peer = e->home_slots > 0;
+  if (peer && !e->peers_ready)
+    return set_error(RK_ERR_VALUE, "peer tier: call rk_engine_load_home and rk_engine_set_peer_homes first");
+  const int world = e->p.world;
   std::vector<rk_pair> pend;
   std::vector<LoadReq> loads;
+  std::vector<LoadReq> fetches;
   std::vector<int32_t> keys;
   std::vector<int32_t> pinned;
+  std::vector<int32_t> slot_of(peer ? n : 0, -1);
   const int lim = batch_limit(e->app);
   for (const Leaf& l : leaves) {
     if (e->app->p.kind == RK_APP_SYNTHETIC) {
@@ -361,6 +375,10 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
     pinned.clear();
     for (int32_t k : keys) {
+      if (peer && k % world == e->p.rank) {
+        slot_of[k] = e->p.device_slots + k / world;   // home item: resident for the whole run
+        continue;
+      }
       const int64_t evictions_before = e->tier->evictions;
       TierResult r = e->tier->acquire(k);
       if (r.kind == kNoEvictable) {
@@ -373,19 +391,35 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
       if (r.kind == kMiss) {
         // the victim may still be read by pairs not yet launched
         if (e->tier->evictions != evictions_before) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
-        loads.push_back(LoadReq{k, r.slot});
+        if (peer) fetches.push_back(LoadReq{k, r.slot});
+        else loads.push_back(LoadReq{k, r.slot});
       }
       pinned.push_back(r.slot);
+      if (peer) slot_of[k] = r.slot;
     }
     RK_TRY(flush_loads(e, loads, h_parsed, d_parsed, parsed_stride));
+    if (!fetches.empty()) {
+      // peer tier hit: copy the preprocessed item from its home GPU over NVLink
+      const size_t sb = e->app->slot_bytes;
+      for (const LoadReq& f : fetches) {
+        const char* src = e->peer_home[f.key % world] + (size_t)(f.key / world) * e->slot_stride;
+        char* dst = static_cast<char*>(e->arena) + (size_t)f.slot * e->slot_stride;
+        RK_CUDA(cudaMemcpyAsync(dst, src, sb, cudaMemcpyDeviceToDevice, e->stream));
+        e->tier->publish(f.slot, true);
+        e->stats.peer_fetches += 1;
+        e->stats.peer_bytes += (int64_t)sb;
+      }
+      fetches.clear();
+    }
     for (int32_t i = l.r0; i < l.r1; ++i)
       for (int32_t j = std::max(l.c0, i + 1); j < l.c1; ++j) {
-        pend.push_back(rk_pair{i, j, e->tier->find(i), e->tier->find(j)});
+        pend.push_back(peer ? rk_pair{i, j, slot_of[i], slot_of[j]} : rk_pair{i, j, e->tier->find(i), e->tier->find(j)});
         if ((int)pend.size() >= lim) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
       }
     for (int s : pinned) e->tier->release(s);
   }
   RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+  (void)world;
   RK_CUDA(cudaStreamSynchronize(e->stream));
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;
@@ -403,6 +437,7 @@ rk_status rk_engine_stats_get(const rk_engine* e, rk_engine_stats* out) {
 rk_status rk_engine_reset_stats(rk_engine* e) {
   if (!e) return set_error(RK_ERR_VALUE, "null engine");
   e->stats = rk_engine_stats{};
+  e->tier->hits = e->tier->misses = e->tier->waits = e->tier->evictions = 0;
   return RK_OK;
 }
 
@@ -423,6 +458,90 @@ rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* s
 }
 
 void* rk_engine_stream(const rk_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Peer-GPU tier: home-item preprocessing and IPC-mapped peer home regions.
+extern "C" {
+
+rk_status rk_engine_home_region(const rk_engine* e, void** d_base, size_t* bytes) {
+  if (!e || !d_base || !bytes) return set_error(RK_ERR_VALUE, "null argument");
+  *d_base = static_cast<char*>(e->arena) + (size_t)e->p.device_slots * e->slot_stride;
+  *bytes = (size_t)e->home_slots * e->slot_stride;
+  return RK_OK;
+}
+
+rk_status rk_engine_arena(const rk_engine* e, void** d_base, size_t* slot_stride) {
+  if (!e || !d_base || !slot_stride) return set_error(RK_ERR_VALUE, "null argument");
+  *d_base = e->arena;
+  *slot_stride = e->slot_stride;
+  return RK_OK;
+}
+
+rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  if (e->home_slots == 0) return set_error(RK_ERR_VALUE, "engine was created without the peer tier");
+  RK_CUDA(cudaSetDevice(e->device));
+  const int32_t n = e->app->p.n;
+  std::vector<LoadReq> home;
+  for (int32_t k = e->p.rank; k < n; k += e->p.world) home.push_back(LoadReq{k, e->p.device_slots + k / e->p.world});
+  // flush_loads publishes into the tier; home slots live outside it, so load directly
+  const size_t pbytes = e->app->parsed_bytes;
+  for (size_t base = 0; base < home.size(); base += e->staging_items) {
+    const int m = (int)std::min<size_t>(e->staging_items, home.size() - base);
+    std::vector<int32_t> slots(m);
+    for (int k = 0; k < m; ++k) slots[k] = home[base + k].slot;
+    // home item m (key rank + m*world) is at parsed + m * parsed_stride
+    if (h_parsed) {
+      for (int k = 0; k < m; ++k) {
+        const char* src = static_cast<const char*>(h_parsed) + (base + k) * parsed_stride;
+        RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->staging) + (size_t)k * pbytes, src, pbytes,
+                                cudaMemcpyHostToDevice, e->stream));
+        e->stats.h2d_bytes += (int64_t)pbytes;
+      }
+      RK_TRY(rk_preprocess(e->app, e->staging, pbytes, m, e->arena, e->slot_stride, slots.data(), e->stream));
+    } else {
+      const char* src = static_cast<const char*>(d_parsed) + base * parsed_stride;
+      RK_TRY(rk_preprocess(e->app, src, parsed_stride, m, e->arena, e->slot_stride, slots.data(), e->stream));
+    }
+    e->stats.loads += m;
+  }
+  RK_CUDA(cudaStreamSynchronize(e->stream));
+  return RK_OK;
+}
+
+rk_status rk_engine_set_peer_homes(rk_engine* e, int32_t world, void* const* d_home_bases) {
+  if (!e || !d_home_bases) return set_error(RK_ERR_VALUE, "null argument");
+  if (world != e->p.world || e->home_slots == 0) return set_error(RK_ERR_VALUE, "peer tier world mismatch");
+  e->peer_home.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) e->peer_home[r] = static_cast<const char*>(d_home_bases[r]);
+  e->peers_ready = true;
+  return RK_OK;
+}
+
+rk_status rk_ipc_handle(const void* d_ptr, uint8_t* out_handle64) {
+  if (!d_ptr || !out_handle64) return set_error(RK_ERR_VALUE, "null argument");
+  cudaIpcMemHandle_t h;
+  RK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(out_handle64, &h, 64);
+  return RK_OK;
+}
+
+rk_status rk_ipc_open(const uint8_t* handle64, int device, void** d_ptr) {
+  if (!handle64 || !d_ptr) return set_error(RK_ERR_VALUE, "null argument");
+  RK_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  RK_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RK_OK;
+}
+
+rk_status rk_ipc_close(void* d_ptr) {
+  RK_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return RK_OK;
+}
 
 }  // extern "C"
 

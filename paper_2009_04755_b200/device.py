@@ -87,11 +87,12 @@ class DeviceEngine:
     """rk_engine: quadtree tiles over an HBM slot tier, fed by host or device items."""
 
     def __init__(self, params: _lib.AppParams, *, leaf_block: int = 8, device_slots: int = 0,
-                 rank: int = 0, world: int = 1, device: int = 0):
+                 rank: int = 0, world: int = 1, device: int = 0, peer_tier: bool = False):
         self.params = params
         self.device = device
+        self.rank, self.world = rank, world
         slots = device_slots if device_slots > 0 else max(2, params.n)
-        ep = _lib.EngineParams(leaf_block, slots, 1, rank, world)
+        ep = _lib.EngineParams(leaf_block, slots, 1, rank, world, int(bool(peer_tier and world > 1)))
         handle = C.c_void_p()
         check(lib.rk_engine_create(C.byref(params), C.byref(ep), device, C.byref(handle)))
         self.handle = handle
@@ -99,6 +100,7 @@ class DeviceEngine:
 
     def close(self) -> None:
         if self.handle:
+            self.close_peers()
             lib.rk_engine_destroy(self.handle)
             self.handle = None
 
@@ -135,3 +137,40 @@ class DeviceEngine:
 
     def stream(self) -> int:
         return int(lib.rk_engine_stream(self.handle) or 0)
+
+    # -- peer-GPU tier (one process per GPU; needs torch.distributed) ----------------
+    @property
+    def peer_tier(self) -> bool:
+        return bool(self.engine_params.peer_tier)
+
+    def load_home(self, *, host_items=None, device_items=None, parsed_stride: int = 0) -> None:
+        check(lib.rk_engine_load_home(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride))
+
+    def connect_peers(self) -> None:
+        """Exchange home regions over CUDA IPC (handles travel through torch.distributed)."""
+        import torch.distributed as dist
+        base, nbytes = C.c_void_p(), C.c_size_t()
+        check(lib.rk_engine_home_region(self.handle, C.byref(base), C.byref(nbytes)))
+        arena, stride = C.c_void_p(), C.c_size_t()
+        check(lib.rk_engine_arena(self.handle, C.byref(arena), C.byref(stride)))
+        hbuf = (C.c_uint8 * 64)()
+        check(lib.rk_ipc_handle(arena, hbuf))
+        mine = (bytes(hbuf), int(base.value) - int(arena.value))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine)
+        ptrs = (C.c_void_p * self.world)()
+        self._opened = []
+        for r, (h, off) in enumerate(everyone):
+            if r == self.rank:
+                ptrs[r] = base.value
+                continue
+            peer = C.c_void_p()
+            check(lib.rk_ipc_open((C.c_uint8 * 64)(*h), self.device, C.byref(peer)))
+            self._opened.append(peer)
+            ptrs[r] = peer.value + off
+        check(lib.rk_engine_set_peer_homes(self.handle, self.world, ptrs))
+
+    def close_peers(self) -> None:
+        for p in getattr(self, "_opened", []):
+            lib.rk_ipc_close(p)
+        self._opened = []

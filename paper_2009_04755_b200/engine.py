@@ -99,14 +99,16 @@ class AllPairsEngine:
     """All pairs of ``app``'s items on one GPU (this rank's share of a multi-GPU job)."""
 
     def __init__(self, app: B200Application, *, leaf_block: int = 16, device_slots: Optional[int] = None,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, peer_tier: bool = True):
         self.app = app
         self.rank = rank
         self.world = world
         torch.cuda.set_device(app.device)
         slots = device_slots if device_slots is not None else app.n
         self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
-                                 rank=rank, world=world, device=app.device)
+                                 rank=rank, world=world, device=app.device,
+                                 peer_tier=peer_tier and world > 1 and app.kind not in (0, 3))
+        self._peers_connected = False
         self._out = torch.empty(app.n * (app.n - 1) // 2, dtype=torch.float64, device=f"cuda:{app.device}")
         self._flags = torch.empty_like(self._out, dtype=torch.uint8)
 
@@ -132,8 +134,32 @@ class AllPairsEngine:
         self._flags.zero_()
         self._eng.reset_stats()
         t0 = time.perf_counter()
+        stride = self.app.parsed_bytes()
+        if self._eng.peer_tier:
+            # home items first (k % world == rank), then the IPC-mapped peer homes
+            import torch.distributed as dist
+            # home item m = key rank + m*world: a strided view of the full item array
+            off = self.rank * stride
+
+            class _At:
+                def __init__(self, t):
+                    self.t = t
+
+                def data_ptr(self):
+                    return self.t.data_ptr() + off
+
+            self._eng.load_home(host_items=None if host_items is None else _At(host_items),
+                                device_items=None if device_items is None else _At(device_items),
+                                parsed_stride=self.world * stride)
+            if not self._peers_connected:
+                self._eng.connect_peers()
+                self._peers_connected = True
+            dist.barrier()   # every home region is complete before anyone reads it
         self._eng.run(self._out, self._flags, host_items=host_items, device_items=device_items,
-                      parsed_stride=self.app.parsed_bytes())
+                      parsed_stride=stride)
+        if self._eng.peer_tier:
+            import torch.distributed as dist
+            dist.barrier()   # peers are done reading our home region
         if self.world > 1 and gather:
             gather_triangle(self._out, self._flags)
         values = self._out.cpu().numpy()
