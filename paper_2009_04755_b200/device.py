@@ -113,6 +113,9 @@ class DeviceEngine:
     def run(self, out: torch.Tensor, flags: Optional[torch.Tensor] = None, *,
             host_items: Optional[torch.Tensor] = None, device_items: Optional[torch.Tensor] = None,
             parsed_stride: int = 0) -> None:
+        # the engine runs on its own stream: order it after the caller's pending work
+        # (e.g. the initialisation of out/flags on torch's stream)
+        torch.cuda.current_stream(self.device).synchronize()
         check(lib.rk_engine_run(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride, _ptr(out),
                                 _ptr(flags)))
 
@@ -144,6 +147,7 @@ class DeviceEngine:
         return bool(self.engine_params.peer_tier)
 
     def load_home(self, *, host_items=None, device_items=None, parsed_stride: int = 0) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
         check(lib.rk_engine_load_home(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride))
 
     def connect_peers(self) -> None:
