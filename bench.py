@@ -45,7 +45,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=4096, help="items (default: configs[1], 4,096)")
     ap.add_argument("--side", type=int, default=1024, help="pattern side (default 1024)")
-    ap.add_argument("--leaf", type=int, default=16)
+    ap.add_argument("--leaf", type=int, default=8)
     ap.add_argument("--cameras", type=int, default=64)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")

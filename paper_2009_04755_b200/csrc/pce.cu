@@ -52,9 +52,16 @@ __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
 
 template <int R>
 struct ClusterShape;
+#ifndef PCE_CL
+#define PCE_CL 1
+#endif
+// Measured on B200 (N = 1024 bench, 1024-pair launches): CL = 8 keeps every T
+// slot L2-resident but only 15 clusters (120 SMs) fit and the per-pair cluster
+// barriers dominate (277k pairs/s); CL = 4: 314k; CL = 2: 376k; CL = 1 (one SM
+// per pair, all 148 SMs, T round-trips through HBM): 383k pairs/s.
 template <>
 struct ClusterShape<32> {
-  static constexpr int CL = 8;   // 15 co-resident clusters on B200: 60 MiB of live T
+  static constexpr int CL = PCE_CL;
 };
 template <>
 struct ClusterShape<16> {
@@ -360,6 +367,18 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   // evict_last; spectra and consumed T stream through with evict_first.
   const uint64_t pol_first = l2_policy_evict_first();
   const uint64_t pol_last = l2_policy_evict_last();
+#ifndef PCE_T_POLICY
+#define PCE_T_POLICY 2
+#endif
+#ifndef PCE_SPEC_POLICY
+#define PCE_SPEC_POLICY 2
+#endif
+  // 0 = evict_last, 1 = evict_first, 2 = evict_normal.  With one pair per SM
+  // (148 T slots, 592 MiB) T cannot stay in L2, so neither T nor the spectra
+  // (reused by the neighbouring pairs of a leaf) get a special priority.
+  const uint64_t pol_T = PCE_T_POLICY == 0 ? pol_last : PCE_T_POLICY == 1 ? pol_first : l2_policy_evict_normal();
+  const uint64_t pol_spec = PCE_SPEC_POLICY == 0 ? pol_last : PCE_SPEC_POLICY == 1 ? pol_first
+                                                                                   : l2_policy_evict_normal();
   cluster_sync();
 
   for (int pi = cid; pi < job.npairs; pi += ncl) {
@@ -378,8 +397,8 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     static_assert(CR * N == kBlk, "a round's column slice fills one tile buffer");
     if (tid == 0) {
       mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-      bulk_g2s_hint(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_first);
-      bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_first);
+      bulk_g2s_hint(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_spec);
+      bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_spec);
     }
 #pragma unroll 1
     for (int c0 = q * NCOL; c0 < (q + 1) * NCOL; c0 += CR) {
@@ -415,8 +434,8 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       if (tid == 0 && c0 + CR < (q + 1) * NCOL) {
         fence_proxy_async();
         mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-        bulk_g2s_hint(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_first);
-        bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_first);
+        bulk_g2s_hint(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_spec);
+        bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_spec);
       }
       group_fft<R, true>(v, xbuf, tw, lane);
       // row lane + R*k2 -> 16-row block (lane>>4) + (R/16)*k2, position lane&15
@@ -425,7 +444,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       float2* dst = Tp + ((size_t)(lane >> 4) * (N / 2) + col) * 16 + pos;
       constexpr size_t kStep = (size_t)(R / 16) * (N / 2) * 16;
 #pragma unroll
-      for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_last);
+      for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
     }
     PCE_PROBE(1);
     cluster_sync();
