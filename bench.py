@@ -371,7 +371,7 @@ def main():
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "traffic": traffic,
                     "traffic_source": "profiles/pce_cluster_traffic.json (ncu dram__bytes_read+write, per launch)",
-                    "kernel": "pce_cluster (persistent 8-CTA cluster per pair: column + row pass)",
+                    "kernel": "pce_cluster (persistent, one CTA = one SM per pair in flight: column + row pass)",
                     "pairs_per_launch": batch, "ms_per_launch": per_launch_ms,
                     "alg_bytes_per_pair": alg_bytes_per_pair, "peak_source": peaks_src,
                     "fp32_flops_per_pair": 2 * 5 * (side // 2) * side * math.log2(side)}
