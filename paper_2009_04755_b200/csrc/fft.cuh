@@ -262,4 +262,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// Same with the lane's twiddles W_N^(lane*k1), k1 = 1..R-1, held in registers
+// (they depend only on the lane): no shared-memory traffic for the twiddle step.
+template <int R, bool INV>
+__device__ __forceinline__ void group_fft_rt(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
+  dft_regs<R, INV>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < R; ++k1) v[k1] = c_mul(v[k1], INV ? c_conj(w[k1]) : w[k1]);
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) xbuf[lane * R + (k1 ^ lane)] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = xbuf[n1 * R + (lane ^ n1)];
+  __syncwarp();
+  dft_regs<R, INV>(v);
+}
+
 }  // namespace rk

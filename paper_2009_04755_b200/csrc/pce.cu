@@ -186,16 +186,45 @@ __global__ void __launch_bounds__(kGroups * R) pce_cols_fwd(const float2* __rest
 }
 
 // ---------------------------------------------------------------------------
-// T (the column pass output) layout per pair: row blocks of 16 rows; block rb
-// holds all N/2 columns x 16 rows, the 16 rows of a column in 128 contiguous
-// bytes with 16-byte chunks XOR-swizzled by (column & 7).  A column FFT stores
-// two 128-B segments per warp instruction; the row pass pulls one 64 KiB block
-// per CTA round with a bulk (TMA) copy and reads row pairs conflict-free.
+// T (the column pass output) layout per pair: blocks of 8 rows; block rb holds
+// all N/2 columns x 8 rows, the 8 rows of one column in 64 contiguous bytes
+// whose four 16-byte row-pair chunks are XOR-swizzled by ((column >> 1) & 3), so
+// eight consecutive columns of one row pair hit eight distinct bank groups.  A
+// column FFT stores four 64-B segments per warp instruction; an 8-row block is
+// one contiguous bulk copy (TMA) feeding four warps, one row pair each.
 template <int N>
-__device__ __forceinline__ size_t t_index(int r, int c) {
-  const int rb = r >> 4, rr = r & 15;
-  const int pos = (((rr >> 1) ^ (c & 7)) << 1) | (rr & 1);
-  return ((size_t)rb * (N / 2) + c) * 16 + pos;
+__device__ __forceinline__ size_t t_index8(int r, int c) {
+  const int rb = r >> 3, rr = r & 7;
+  const int pos = (((rr >> 1) ^ ((c >> 1) & 3)) << 1) | (rr & 1);
+  return ((size_t)rb * (N / 2) + c) * 8 + pos;
+}
+
+// Z[k] = A[k] + i*B[k] for row pair rp (rows 2rp, 2rp+1) of a staged 8-row block
+// ([c][8] with the chunk swizzle), Hermitian-extended; column 0 packs DC + i*Nyquist.
+template <int R>
+__device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk, int rp, int lane) {
+  constexpr int N = R * R;
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) {
+    const int k = lane + R * n2;
+    int kk = (n2 < R / 2) ? k : N - k;
+    if (kk >= N / 2) kk = 0;   // lane 0 at k = N/2: the Nyquist value lives in column 0
+    const float4 q = *reinterpret_cast<const float4*>(blk + kk * 8 + 2 * (rp ^ ((kk >> 1) & 3)));
+    float2 a = make_float2(q.x, q.y), c = make_float2(q.z, q.w);
+    if (n2 >= R / 2) {
+      a.y = -a.y;
+      c.y = -c.y;
+    }
+    if (kk == 0) {
+      a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
+      c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
+    }
+    v[n2] = make_float2(a.x - c.y, a.y + c.x);
+  }
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 struct ArgMax {
@@ -221,56 +250,6 @@ __device__ __forceinline__ T warp_sum(T x) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
-}
-
-// Hermitian-extended spectrum Z[k] = A[k] + i*B[k] of rows (ra, rb) of T at
-// k = lane + R*n2 (rows of N/2 complex values; column 0 packs DC + i*Nyquist).
-template <int R>
-__device__ __forceinline__ void load_rows_z(float2 (&v)[R], const float2* __restrict__ Tp, int ra, int rb,
-                                            bool has_b, int lane, uint64_t pol) {
-  constexpr int N = R * R;
-#pragma unroll
-  for (int n2 = 0; n2 < R; ++n2) {
-    const int k = lane + R * n2;
-    int kk = (n2 < R / 2) ? k : N - k;
-    if (kk >= N / 2) kk = 0;   // lane 0 at k = N/2: the Nyquist value lives in column 0
-    const float2 ta = ldg_hint(Tp + t_index<N>(ra, kk), pol);
-    const float2 tb = has_b ? ldg_hint(Tp + t_index<N>(rb, kk), pol) : make_float2(0.f, 0.f);
-    float2 x = ta, c = tb;
-    if (n2 >= R / 2) {
-      x.y = -x.y;
-      c.y = -c.y;
-    }
-    if (kk == 0) {
-      x = make_float2(n2 == 0 ? ta.x : ta.y, 0.f);
-      c = make_float2(n2 == 0 ? tb.x : tb.y, 0.f);
-    }
-    v[n2] = make_float2(x.x - c.y, x.y + c.x);
-  }
-}
-
-// Same from a 16-row block staged in shared memory: row pair cr (rows 2cr, 2cr+1)
-// is one 16-byte chunk per frequency (conflict-free LDS.128 across 8 lanes).
-template <int R>
-__device__ __forceinline__ void block_rows_z(float2 (&v)[R], const float2* tile, int cr, int lane) {
-  constexpr int N = R * R;
-#pragma unroll
-  for (int n2 = 0; n2 < R; ++n2) {
-    const int k = lane + R * n2;
-    int kk = (n2 < R / 2) ? k : N - k;
-    if (kk >= N / 2) kk = 0;
-    const float4 q = *reinterpret_cast<const float4*>(tile + kk * 16 + 2 * (cr ^ (kk & 7)));
-    float2 a = make_float2(q.x, q.y), c = make_float2(q.z, q.w);
-    if (n2 >= R / 2) {
-      a.y = -a.y;
-      c.y = -c.y;
-    }
-    if (kk == 0) {
-      a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
-      c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
-    }
-    v[n2] = make_float2(a.x - c.y, a.y + c.x);
-  }
 }
 
 // Running (max, first index, sum of squares) over one row pair of C.
@@ -323,20 +302,22 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
   constexpr int kCtaWarps = cta_warps(R);
-  constexpr int CR = kCtaWarps * G;       // columns per CTA round (one per lane group)
   constexpr int NT = kCtaWarps * 32;
+  constexpr int kGW = kCtaWarps / 2;      // warps per warp group (two independent groups)
+  constexpr int kGL = kGW * G;            // lane groups per warp group: 4 columns / 4 row pairs per round
   constexpr int NCOL = (N / 2) / CL;      // columns per CTA
-  constexpr int NRP = (N / 2) / CL;       // row pairs per CTA
+  constexpr int NB8 = (N / 8) / CL;       // 8-row blocks per CTA
   constexpr int kPairsOfRows = (kWin + 1) / 2;
-  static_assert(NCOL * CL == N / 2 && NCOL % CR == 0 && NRP % 8 == 0 && CR == 8, "cluster split");
-  constexpr int kBlk = (N / 2) * 16;      // float2 per 16-row block of T
-  constexpr uint32_t kBlkBytes = kBlk * sizeof(float2);
-  constexpr int NB = NRP / 8;             // row blocks per CTA
+  constexpr int kHalf = 4 * N;            // float2: 4 columns of a slot == one 8-row block of T
+  constexpr uint32_t kHalfBytes = kHalf * sizeof(float2);
+  static_assert(kGL == 4, "a warp group owns 4 lane groups");
+  static_assert(NCOL * CL == N / 2 && NCOL % 8 == 0 && NB8 * CL == N / 8 && NB8 % 2 == 0, "cluster split");
   extern __shared__ __align__(128) float2 smem[];
-  float2* tiles = smem;                   // 2 x 16-row blocks (bulk-copy double buffer)
-  float2* tw = smem + 2 * kBlk;           // R*R twiddles
+  float2* gbufs = smem;                   // 2 groups x 2 halves of 4N float2 (column slices / row blocks)
+  float2* tw = smem + 4 * kHalf;          // R*R twiddles
   float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
-  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_bar[2][3];   // per group: column slices, row block 0 / 1
+  __shared__ __align__(8) uint64_t s_wbar;
   __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
   __shared__ float s_wpart[8];            // window energy per row pair, gathered in CTA 0
   __shared__ float s_v[kCtaWarps];
@@ -349,36 +330,43 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   const int tid = threadIdx.x;
   const int warp = tid >> 5, wl = tid & 31;
   const int g = wl / R, lane = wl % R;
-  const int grp = warp * G + g;
+  const int grp = warp * G + g;           // lane group in the CTA
+  const int wg = warp / kGW;              // warp group 0 / 1
+  const int gi = (warp % kGW) * G + g;    // lane group within the warp group, 0..3
+  const bool leader = (tid % (kGW * 32)) == 0;
   const int q = (int)cluster_ctarank();
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   float2* xbuf = xbufs + grp * R * R;
+  float2* gb = gbufs + wg * 2 * kHalf;    // this warp group's 2 x 4N float2
   float2* Tp = T + (size_t)cid * (N / 2) * N;
   for (int i = tid; i < R * R; i += NT) tw[i] = tw_g[i];
   if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+    for (int w = 0; w < 2; ++w)
+      for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
+    mbar_init(&s_wbar, 1);
   }
-  uint32_t bar_phase = 0;                 // bit b: parity of s_bar[b]
+  uint32_t ph = 0;                        // parity bits of this group's three barriers (bit b)
+  uint32_t wph = 0;
   __syncthreads();
   const uint32_t part0 = dsmem_addr(&s_part[0], 0);
   const uint32_t wpart0 = dsmem_addr(&s_wpart[0], 0);
-  // L2 residency: T (written, then read once by the row phase) is kept with
-  // evict_last; spectra and consumed T stream through with evict_first.
-  const uint64_t pol_first = l2_policy_evict_first();
-  const uint64_t pol_last = l2_policy_evict_last();
+  float2 twr[R];   // this lane's twiddles W_N^(lane*k1): no shared-memory traffic in the FFTs
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) twr[k1] = tw[k1 * R + lane];
 #ifndef PCE_T_POLICY
 #define PCE_T_POLICY 2
 #endif
 #ifndef PCE_SPEC_POLICY
 #define PCE_SPEC_POLICY 2
 #endif
-  // 0 = evict_last, 1 = evict_first, 2 = evict_normal.  With one pair per SM
-  // (148 T slots, 592 MiB) T cannot stay in L2, so neither T nor the spectra
+  // L2 priority (0 = evict_last, 1 = evict_first, 2 = evict_normal).  With one pair
+  // per SM (148 T slots, 592 MiB) T cannot stay in L2, so neither T nor the spectra
   // (reused by the neighbouring pairs of a leaf) get a special priority.
-  const uint64_t pol_T = PCE_T_POLICY == 0 ? pol_last : PCE_T_POLICY == 1 ? pol_first : l2_policy_evict_normal();
-  const uint64_t pol_spec = PCE_SPEC_POLICY == 0 ? pol_last : PCE_SPEC_POLICY == 1 ? pol_first
-                                                                                   : l2_policy_evict_normal();
+  const uint64_t pol_first = l2_policy_evict_first();
+  const uint64_t pol_T = PCE_T_POLICY == 0 ? l2_policy_evict_last()
+                         : PCE_T_POLICY == 1 ? pol_first : l2_policy_evict_normal();
+  const uint64_t pol_spec = PCE_SPEC_POLICY == 0 ? l2_policy_evict_last()
+                            : PCE_SPEC_POLICY == 1 ? pol_first : l2_policy_evict_normal();
   cluster_sync();
 
   for (int pi = cid; pi < job.npairs; pi += ncl) {
@@ -386,96 +374,105 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     float2 v[R];
     PCE_PROBE(0);
 
-    // ---------------- column phase: NCOL columns in rounds of CR ----------------
-    // X and Y column slices of a round (CR consecutive columns, contiguous in the
-    // slots) are bulk-copied into the two tile buffers; the next round's copy is
-    // issued as soon as every group has formed its product, so it lands while
-    // the FFTs run.
+    // ---------------- column phase ----------------
+    // Two warp groups run independently (named barriers), each streaming 4-column
+    // slices of X and Y (contiguous in the slots) through its own buffer; a slice
+    // is refilled as soon as the group has formed its products, so the copy lands
+    // while the FFTs run, and the two groups' smem-heavy and FMA-heavy steps interleave.
     const float2* Xs = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_a * slot_stride);
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
-    constexpr uint32_t kColBytes = (uint32_t)CR * N * sizeof(float2);
-    static_assert(CR * N == kBlk, "a round's column slice fills one tile buffer");
-    if (tid == 0) {
-      mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-      bulk_g2s_hint(tiles, Xs + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_spec);
-      bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(q * NCOL) * N, kColBytes, &s_bar[0], pol_spec);
-    }
-#pragma unroll 1
-    for (int c0 = q * NCOL; c0 < (q + 1) * NCOL; c0 += CR) {
-      const int col = c0 + grp;
-      mbar_wait(&s_bar[0], bar_phase & 1u);
-      bar_phase ^= 1u;
-      const float2* X = tiles + grp * N;
-      const float2* Y = tiles + kBlk + grp * N;
-      if (col != 0) {
-#pragma unroll
-        for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(X[lane + R * n2], Y[lane + R * n2]);
-      } else {
-        // packed DC/Nyquist column: split both sides into their Hermitian parts,
-        // multiply separately, re-pack the (Hermitian) products
-#pragma unroll
-        for (int n2 = 0; n2 < R; ++n2) {
-          const int m = lane + R * n2;
-          const int mm = (N - m) & (N - 1);
-          const float2 x = X[m], xr = c_conj(X[mm]);
-          const float2 y = Y[m], yr = c_conj(Y[mm]);
-          const float2 xa = c_scale(c_add(x, xr), 0.5f);
-          const float2 dx = c_sub(x, xr);
-          const float2 xb = make_float2(0.5f * dx.y, -0.5f * dx.x);
-          const float2 ya = c_scale(c_add(y, yr), 0.5f);
-          const float2 dy = c_sub(y, yr);
-          const float2 yb = make_float2(0.5f * dy.y, -0.5f * dy.x);
-          const float2 pa = c_mulc(xa, ya);
-          const float2 pb = c_mulc(xb, yb);
-          v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
-        }
-      }
-      __syncthreads();   // the round's slices are consumed
-      if (tid == 0 && c0 + CR < (q + 1) * NCOL) {
+    {
+      const int cbeg = q * NCOL + 4 * wg, cend = (q + 1) * NCOL;
+      uint64_t* bar = &s_bar[wg][0];
+      if (leader) {
         fence_proxy_async();
-        mbar_expect_tx(&s_bar[0], 2 * kColBytes);
-        bulk_g2s_hint(tiles, Xs + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_spec);
-        bulk_g2s_hint(tiles + kBlk, Ys + (size_t)(c0 + CR) * N, kColBytes, &s_bar[0], pol_spec);
+        mbar_expect_tx(bar, 2 * kHalfBytes);
+        bulk_g2s_hint(gb, Xs + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
+        bulk_g2s_hint(gb + kHalf, Ys + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
       }
-      group_fft<R, true>(v, xbuf, tw, lane);
-      // row lane + R*k2 -> 16-row block (lane>>4) + (R/16)*k2, position lane&15
-      const int rr = lane & 15;
-      const int pos = (((rr >> 1) ^ (col & 7)) << 1) | (rr & 1);
-      float2* dst = Tp + ((size_t)(lane >> 4) * (N / 2) + col) * 16 + pos;
-      constexpr size_t kStep = (size_t)(R / 16) * (N / 2) * 16;
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        const int col = c0 + gi;
+        mbar_wait(bar, ph & 1u);
+        ph ^= 1u;
+        const float2* X = gb + gi * N;
+        const float2* Y = gb + kHalf + gi * N;
+        if (col != 0) {
 #pragma unroll
-      for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
+          for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(X[lane + R * n2], Y[lane + R * n2]);
+        } else {
+          // packed DC/Nyquist column: split both sides into their Hermitian parts,
+          // multiply separately, re-pack the (Hermitian) products
+#pragma unroll
+          for (int n2 = 0; n2 < R; ++n2) {
+            const int m = lane + R * n2;
+            const int mm = (N - m) & (N - 1);
+            const float2 x = X[m], xr = c_conj(X[mm]);
+            const float2 y = Y[m], yr = c_conj(Y[mm]);
+            const float2 xa = c_scale(c_add(x, xr), 0.5f);
+            const float2 dx = c_sub(x, xr);
+            const float2 xb = make_float2(0.5f * dx.y, -0.5f * dx.x);
+            const float2 ya = c_scale(c_add(y, yr), 0.5f);
+            const float2 dy = c_sub(y, yr);
+            const float2 yb = make_float2(0.5f * dy.y, -0.5f * dy.x);
+            const float2 pa = c_mulc(xa, ya);
+            const float2 pb = c_mulc(xb, yb);
+            v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
+          }
+        }
+        named_bar(1 + wg, kGW * 32);   // this group's slices are consumed
+        if (leader && c0 + 8 < cend) {
+          fence_proxy_async();
+          mbar_expect_tx(bar, 2 * kHalfBytes);
+          bulk_g2s_hint(gb, Xs + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
+          bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
+        }
+        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
+        const int rr = lane & 7;
+        const int pos = (((rr >> 1) ^ ((col >> 1) & 3)) << 1) | (rr & 1);
+        float2* dst = Tp + ((size_t)(lane >> 3) * (N / 2) + col) * 8 + pos;
+        constexpr size_t kStep = (size_t)(R / 8) * (N / 2) * 8;
+#pragma unroll
+        for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
+      }
     }
     PCE_PROBE(1);
     cluster_sync();
     PCE_PROBE(2);
 
-    // ---------------- row phase: NB 16-row blocks, bulk-copied, double-buffered ----------------
-    const int blk0 = q * NB;   // first 16-row block of this CTA
-    if (tid == 0) {
-      fence_proxy_async();     // T's generic-proxy writes (ordered by the cluster barrier) -> async proxy
-      for (int b = 0; b < 2 && b < NB; ++b) {
-        mbar_expect_tx(&s_bar[b], kBlkBytes);
-        bulk_g2s_hint(tiles + b * kBlk, Tp + (size_t)(blk0 + b) * kBlk, kBlkBytes, &s_bar[b], pol_first);
-      }
-    }
+    // ---------------- row phase ----------------
+    // Each warp group streams its 8-row blocks (one row pair per lane group)
+    // through a double buffer of bulk copies.
     float m = -INFINITY, ss = 0.f;
     int idx = 0x7fffffff;
-#pragma unroll 1
-    for (int b = 0; b < NB; ++b) {
-      const int buf = b & 1;
-      mbar_wait(&s_bar[buf], (bar_phase >> buf) & 1u);
-      bar_phase ^= 1u << buf;
-      const int cr = grp;                     // row pair within the block (CR == 8 row pairs)
-      block_rows_z<R>(v, tiles + buf * kBlk, cr, lane);
-      __syncthreads();                        // the block is consumed: refill it
-      if (tid == 0 && b + 2 < NB) {
-        fence_proxy_async();
-        mbar_expect_tx(&s_bar[buf], kBlkBytes);
-        bulk_g2s_hint(tiles + buf * kBlk, Tp + (size_t)(blk0 + b + 2) * kBlk, kBlkBytes, &s_bar[buf], pol_first);
+    {
+      const int bbeg = q * NB8 + wg, bend = (q + 1) * NB8;
+      if (leader) {
+        fence_proxy_async();     // T's generic-proxy stores (ordered by the cluster barrier) -> async proxy
+        for (int b = 0; b < 2 && bbeg + 2 * b < bend; ++b) {
+          mbar_expect_tx(&s_bar[wg][1 + b], kHalfBytes);
+          bulk_g2s_hint(gb + b * kHalf, Tp + (size_t)(bbeg + 2 * b) * kHalf, kHalfBytes, &s_bar[wg][1 + b],
+                        pol_first);
+        }
       }
-      group_fft<R, true>(v, xbuf, tw, lane);
-      argmax_update<R>(v, 2 * (8 * (blk0 + b) + cr), lane, m, idx, ss);
+      int it = 0;
+#pragma unroll 1
+      for (int rb = bbeg; rb < bend; rb += 2, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&s_bar[wg][1 + buf], (ph >> (1 + buf)) & 1u);
+        ph ^= 2u << buf;
+        block8_rows_z<R>(v, gb + buf * kHalf, gi, lane);
+        named_bar(1 + wg, kGW * 32);   // the block is consumed: refill it
+        if (leader && rb + 4 < bend) {
+          fence_proxy_async();
+          mbar_expect_tx(&s_bar[wg][1 + buf], kHalfBytes);
+          bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 4) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
+                        pol_first);
+        }
+        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        argmax_update<R>(v, 8 * rb + 2 * gi, lane, m, idx, ss);
+      }
     }
     PCE_PROBE(3);
     {
@@ -515,26 +512,48 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     __syncthreads();
 
     // ---------------- window: 11 rows around the peak ----------------
+    // The 6 aligned row pairs covering rows peak-5 .. peak+5 lie in at most three
+    // 8-row blocks: bulk-copy them into the (now free) group buffers, then six warps
+    // (spread over the cluster) recompute one row pair each.
     {
       const int prow = s_pidx / N, pcol = s_pidx % N;
-      const int t = q + CL * warp;   // one row pair per warp: t = 0..5
-      if (t < kPairsOfRows) {
-        const bool has_b = (2 * t + 1) < kWin && g == 0;
-        const int rowa = (prow - kHalfWin + 2 * t + N) & (N - 1);
-        const int rowb = (prow - kHalfWin + 2 * t + 1 + N) & (N - 1);
-        load_rows_z<R>(v, Tp, rowa, rowb, has_b, lane, pol_first);
+      const int rstart = (prow - kHalfWin + N) & (N - 1);
+      const int e0 = rstart & ~1;                              // first aligned row of the 12-row span
+      const int b0 = e0 >> 3;
+      const int t = q + CL * warp;                             // row pair t = 0..5 of the span
+      const bool mine = (t < kPairsOfRows);
+      // blocks b0, b0+1, b0+2 (mod N/8) -> buffer slots 0..2 (each 4N float2)
+      bool any = false;
+      for (int w = 0; w < kCtaWarps; ++w) any |= (q + CL * w) < kPairsOfRows;
+      if (any) {
+        if (tid == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(&s_wbar, 3 * kHalfBytes);
+          for (int j = 0; j < 3; ++j)
+            bulk_g2s_hint(gbufs + j * kHalf, Tp + (size_t)((b0 + j) & (N / 8 - 1)) * kHalf, kHalfBytes, &s_wbar,
+                          pol_first);
+        }
+        mbar_wait(&s_wbar, wph & 1u);
+        wph ^= 1u;
+      }
+      if (mine) {
+        const int ra = (e0 + 2 * t) & (N - 1);                // even row: pair (ra, ra + 1)
+        const int j = ((ra >> 3) - b0 + (N / 8)) & (N / 8 - 1);   // which staged block
+        block8_rows_z<R>(v, gbufs + j * kHalf, (ra & 7) >> 1, lane);
         if (g != 0) {   // R = 16: the warp's second lane group has no row pair
 #pragma unroll
           for (int n2 = 0; n2 < R; ++n2) v[n2] = make_float2(0.f, 0.f);
         }
-        group_fft<R, true>(v, xbuf, tw, lane);
+        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        const bool va = ((ra - rstart + N) & (N - 1)) < kWin;
+        const bool vb = ((ra + 1 - rstart + N) & (N - 1)) < kWin;
         float w = 0.f;
 #pragma unroll
         for (int k2 = 0; k2 < R; ++k2) {
           const int s = lane + R * k2;
           if (((s - pcol + kHalfWin + N) & (N - 1)) < kWin) {
-            w = fmaf(v[k2].x, v[k2].x, w);
-            w = fmaf(v[k2].y, v[k2].y, w);   // zero for the padding row
+            if (va) w = fmaf(v[k2].x, v[k2].x, w);
+            if (vb) w = fmaf(v[k2].y, v[k2].y, w);
           }
         }
         w = warp_sum(w);
@@ -568,7 +587,8 @@ size_t rows_fwd_smem() {
 template <int R>
 size_t cluster_smem() {
   constexpr int N = R * R;
-  return (size_t)(2 * (N / 2) * 16 + R * R + cta_warps(R) * (32 / R) * R * R) * sizeof(float2);
+  // 2 warp groups x 2 x 4N (column slices / 8-row blocks) + twiddles + one transpose per lane group
+  return (size_t)(16 * N + R * R + cta_warps(R) * (32 / R) * R * R) * sizeof(float2);
 }
 
 template <int R>
