@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librocket.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["capi.cpp", "engine.cpp", "pce.cu", "synthetic.cu", "cv.cu", "ncc.cu", "gmm.cu"]
+SOURCES = ["capi.cpp", "engine.cpp", "pce.cu", "pce2k.cu", "synthetic.cu", "cv.cu", "ncc.cu", "gmm.cu"]
 
 
 def _nvcc() -> str:

@@ -259,7 +259,7 @@ class B200Application(Application):
 class PCEApp(B200Application):
     """PRNU peak-to-correlation-energy over fp32 patterns (forensics).
 
-    Items are square fp32 patterns (256^2 or 1024^2).  By default they are the
+    Items are square fp32 patterns (256^2, 1024^2 or 2048^2).  By default they are the
     deterministic synthetic PRNU-like patterns of rk_synth_prnu (item k =
     0.2*K[k % cameras] + N(0,1)); pass ``patterns`` (n x side x side float32) to
     compare real data.  postprocess: match = PCE >= threshold (default 60).

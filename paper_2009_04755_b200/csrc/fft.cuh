@@ -69,6 +69,62 @@ __device__ __forceinline__ float2 tw32_mul(float2 d, int m) {
   return c_mul(d, w);
 }
 
+// (cos, sin)(2*pi*m/64) for m in [0, 32); m is a compile-time constant after unrolling.
+__device__ __forceinline__ float2 unit64(int m) {
+  switch (m) {
+    case 1: return make_float2(9.951847267e-01f, 9.801714033e-02f);
+    case 2: return make_float2(9.807852804e-01f, 1.950903220e-01f);
+    case 3: return make_float2(9.569403357e-01f, 2.902846773e-01f);
+    case 4: return make_float2(9.238795325e-01f, 3.826834324e-01f);
+    case 5: return make_float2(8.819212643e-01f, 4.713967368e-01f);
+    case 6: return make_float2(8.314696123e-01f, 5.555702330e-01f);
+    case 7: return make_float2(7.730104534e-01f, 6.343932842e-01f);
+    case 8: return make_float2(7.071067812e-01f, 7.071067812e-01f);
+    case 9: return make_float2(6.343932842e-01f, 7.730104534e-01f);
+    case 10: return make_float2(5.555702330e-01f, 8.314696123e-01f);
+    case 11: return make_float2(4.713967368e-01f, 8.819212643e-01f);
+    case 12: return make_float2(3.826834324e-01f, 9.238795325e-01f);
+    case 13: return make_float2(2.902846773e-01f, 9.569403357e-01f);
+    case 14: return make_float2(1.950903220e-01f, 9.807852804e-01f);
+    case 15: return make_float2(9.801714033e-02f, 9.951847267e-01f);
+    case 16: return make_float2(6.123233996e-17f, 1.000000000e+00f);
+    case 17: return make_float2(-9.801714033e-02f, 9.951847267e-01f);
+    case 18: return make_float2(-1.950903220e-01f, 9.807852804e-01f);
+    case 19: return make_float2(-2.902846773e-01f, 9.569403357e-01f);
+    case 20: return make_float2(-3.826834324e-01f, 9.238795325e-01f);
+    case 21: return make_float2(-4.713967368e-01f, 8.819212643e-01f);
+    case 22: return make_float2(-5.555702330e-01f, 8.314696123e-01f);
+    case 23: return make_float2(-6.343932842e-01f, 7.730104534e-01f);
+    case 24: return make_float2(-7.071067812e-01f, 7.071067812e-01f);
+    case 25: return make_float2(-7.730104534e-01f, 6.343932842e-01f);
+    case 26: return make_float2(-8.314696123e-01f, 5.555702330e-01f);
+    case 27: return make_float2(-8.819212643e-01f, 4.713967368e-01f);
+    case 28: return make_float2(-9.238795325e-01f, 3.826834324e-01f);
+    case 29: return make_float2(-9.569403357e-01f, 2.902846773e-01f);
+    case 30: return make_float2(-9.807852804e-01f, 1.950903220e-01f);
+    case 31: return make_float2(-9.951847267e-01f, 9.801714033e-02f);
+    default: return make_float2(1.0f, 0.0f);
+  }
+}
+
+// Last radix-2 step of a 2M-point FFT (M = R*R, R = 32) from the M-point FFTs of
+// its even (e) and odd (o) samples, both in group_fft's lane + R*k1 order:
+//   X[k] = E[k] + W^k O[k],  X[k + M] = E[k] - W^k O[k],  W = exp(-+2*pi*i/2M),
+// with W^k = W^lane * W_64^k1 (wl = W^lane, forward sign).  On exit e holds
+// X[lane + R*k1] and o holds X[M + lane + R*k1].
+template <bool INV>
+__device__ __forceinline__ void radix2_last(float2 (&e)[32], float2 (&o)[32], float2 wl) {
+  if (INV) wl.y = -wl.y;
+#pragma unroll
+  for (int k1 = 0; k1 < 32; ++k1) {
+    float2 w = unit64(k1);
+    if (!INV) w.y = -w.y;
+    const float2 t = c_mul(o[k1], k1 == 0 ? wl : c_mul(wl, w));
+    o[k1] = c_sub(e[k1], t);
+    e[k1] = c_add(e[k1], t);
+  }
+}
+
 __host__ __device__ constexpr int bitrev_const(int i, int logn) {
   int r = 0;
   for (int b = 0; b < logn; ++b) r |= ((i >> b) & 1) << (logn - 1 - b);
@@ -274,6 +330,31 @@ __device__ __forceinline__ void group_fft_rt(float2 (&v)[R], float2* xbuf, const
   __syncwarp();
 #pragma unroll
   for (int n1 = 0; n1 < R; ++n1) v[n1] = xbuf[n1 * R + (lane ^ n1)];
+  __syncwarp();
+  dft_regs<R, INV>(v);
+}
+
+// Same transform with a padded (stride R + 1) transpose buffer of R*(R+1) float2:
+// every transpose address is the lane's base plus a compile-time offset, so the
+// unrolled stores/loads carry no per-element address registers (the XOR swizzle
+// above needs R of them, which spill under 255-register pressure).  Conflict-free
+// for R = 32 (64-bit accesses are split into half-warp wavefronts).
+template <int R, bool INV>
+__device__ __forceinline__ void group_fft_pad(float2 (&v)[R], float2* xbuf, const float2* __restrict__ tw, int lane) {
+  dft_regs<R, INV>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < R; ++k1) {
+    float2 w = tw[k1 * R + lane];
+    if (INV) w.y = -w.y;
+    v[k1] = c_mul(v[k1], w);
+  }
+  float2* wr = xbuf + lane * (R + 1);
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) wr[k1] = v[k1];
+  __syncwarp();
+  const float2* rd = xbuf + lane;
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = rd[n1 * (R + 1)];
   __syncwarp();
   dft_regs<R, INV>(v);
 }

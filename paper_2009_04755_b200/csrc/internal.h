@@ -60,7 +60,7 @@ struct PceJob {
   DevPair pairs[kPipeMaxPairs];
 };
 struct PceState {
-  int R = 0;               // group width; N = R*R
+  int R = 0;               // group width; N = R*R (R = 32 and N = 2048: two warp FFTs per line)
   int N = 0;               // pattern side
   int batch = 0;           // items per preprocess launch
   float2* tw = nullptr;    // [k1][n1] W_N^(n1*k1), R*R entries
@@ -96,6 +96,14 @@ void pce_free(rk_app* app);
 rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items,
                          void* d_slots, size_t slot_stride, const int32_t* h_slot_idx,
                          cudaStream_t s);
+
+// 2048^2 variant (pce2k.cu) and the shared mean-reduction launch (pce.cu)
+rk_status pce2k_init(rk_app* app);
+rk_status pce2k_preprocess(rk_app* app, const float* pix, size_t stride_f, int n_items, char* slots,
+                           size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s);
+rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, const rk_pair* pairs, int n,
+                        double* d_out, uint8_t* d_flags, cudaStream_t s);
+void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, float* mean_part, cudaStream_t s);
 
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s);

@@ -35,18 +35,17 @@
 #include <algorithm>
 
 #include "fft.cuh"
+#include "pce_common.cuh"
 #include "internal.h"
 
 namespace rk {
 
 namespace {
+using namespace pcek;
 
 constexpr int kGroups = 8;              // FFT groups (row-pairs / columns) per preprocess CTA
 constexpr int kRows = 2 * kGroups;      // rows per preprocess row-pass CTA
 constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] tile
-constexpr int kMeanParts = 64;          // CTAs per item in the mean reduction
-constexpr int kWin = 11;                // PCE exclusion neighbourhood side
-constexpr int kHalfWin = kWin / 2;
 // warps per compare CTA: 8 lane groups (one per row pair of a 16-row block); one CTA per SM
 __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
 
@@ -67,10 +66,6 @@ template <>
 struct ClusterShape<16> {
   static constexpr int CL = 2;
 };
-
-__device__ __forceinline__ bool better(float v, int idx, float bv, int bidx) {
-  return v > bv || (v == bv && idx < bidx);
-}
 
 // ---------------------------------------------------------------------------
 // Preprocess P0: per-item partial sums for the mean.
@@ -183,101 +178,6 @@ __global__ void __launch_bounds__(kGroups * R) pce_cols_fwd(const float2* __rest
   constexpr float kScale = 1.0f / (float)N;
 #pragma unroll
   for (int k2 = 0; k2 < R; ++k2) S[lane + R * k2] = c_scale(v[k2], kScale);
-}
-
-// ---------------------------------------------------------------------------
-// T (the column pass output) layout per pair: blocks of 8 rows; block rb holds
-// all N/2 columns x 8 rows, the 8 rows of one column in 64 contiguous bytes
-// whose four 16-byte row-pair chunks are XOR-swizzled by ((column >> 1) & 3), so
-// eight consecutive columns of one row pair hit eight distinct bank groups.  A
-// column FFT stores four 64-B segments per warp instruction; an 8-row block is
-// one contiguous bulk copy (TMA) feeding four warps, one row pair each.
-template <int N>
-__device__ __forceinline__ size_t t_index8(int r, int c) {
-  const int rb = r >> 3, rr = r & 7;
-  const int pos = (((rr >> 1) ^ ((c >> 1) & 3)) << 1) | (rr & 1);
-  return ((size_t)rb * (N / 2) + c) * 8 + pos;
-}
-
-// Z[k] = A[k] + i*B[k] for row pair rp (rows 2rp, 2rp+1) of a staged 8-row block
-// ([c][8] with the chunk swizzle), Hermitian-extended; column 0 packs DC + i*Nyquist.
-template <int R>
-__device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk, int rp, int lane) {
-  constexpr int N = R * R;
-#pragma unroll
-  for (int n2 = 0; n2 < R; ++n2) {
-    const int k = lane + R * n2;
-    int kk = (n2 < R / 2) ? k : N - k;
-    if (kk >= N / 2) kk = 0;   // lane 0 at k = N/2: the Nyquist value lives in column 0
-    const float4 q = *reinterpret_cast<const float4*>(blk + kk * 8 + 2 * (rp ^ ((kk >> 1) & 3)));
-    float2 a = make_float2(q.x, q.y), c = make_float2(q.z, q.w);
-    if (n2 >= R / 2) {
-      a.y = -a.y;
-      c.y = -c.y;
-    }
-    if (kk == 0) {
-      a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
-      c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
-    }
-    v[n2] = make_float2(a.x - c.y, a.y + c.x);
-  }
-}
-
-__device__ __forceinline__ void named_bar(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-struct ArgMax {
-  float v;
-  int idx;
-};
-
-__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, a.v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, a.idx, o);
-    if (better(ov, oi, a.v, a.idx)) {
-      a.v = ov;
-      a.idx = oi;
-    }
-  }
-  return a;
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T x) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
-// Running (max, first index, sum of squares) over one row pair of C.
-template <int R>
-__device__ __forceinline__ void argmax_update(const float2 (&v)[R], int ra, int lane, float& m, int& idx, float& ss) {
-  constexpr int N = R * R;
-  float lm = -INFINITY;
-#pragma unroll
-  for (int k2 = 0; k2 < R; ++k2) {
-    ss = fmaf(v[k2].x, v[k2].x, ss);
-    ss = fmaf(v[k2].y, v[k2].y, ss);
-    lm = fmaxf(lm, fmaxf(v[k2].x, v[k2].y));
-  }
-  if (lm >= m) {
-    int li = 0x7fffffff;
-#pragma unroll
-    for (int k2 = R - 1; k2 >= 0; --k2)
-      if (v[k2].x == lm) li = ra * N + lane + R * k2;
-    if (li == 0x7fffffff) {
-#pragma unroll
-      for (int k2 = R - 1; k2 >= 0; --k2)
-        if (v[k2].y == lm) li = (ra + 1) * N + lane + R * k2;
-    }
-    if (lm > m || li < idx) {
-      m = lm;
-      idx = li;
-    }
-  }
 }
 
 // Optional phase timing (compile with -DPCE_PROBES): per (CTA, warp 0|last) and
@@ -676,12 +576,17 @@ rk_status cluster_init(rk_app* app) {
 
 }  // namespace
 
+void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, float* mean_part, cudaStream_t s) {
+  pce_mean_partial<<<dim3(kMeanParts, n_items), 256, 0, s>>>(pix, stride_f, nn, mean_part);
+}
+
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s) {
   const char* slots = static_cast<const char*>(d_slots);
   for (int base = 0; base < n; base += kPipeMaxPairs) {
     const int m = std::min(kPipeMaxPairs, n - base);
-    if (app->pce.R == 16) RK_TRY(compare_impl<16>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
+    if (app->pce.N == 2048) RK_TRY(pce2k_compare(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
+    else if (app->pce.R == 16) RK_TRY(compare_impl<16>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
     else RK_TRY(compare_impl<32>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
   }
   return RK_OK;
@@ -693,11 +598,12 @@ rk_status pce_init(rk_app* app) {
   int R = 0;
   if (h == 256) R = 16;
   else if (h == 1024) R = 32;
-  else return set_error(RK_ERR_UNSUPPORTED, "PCE pattern side %d not built (256 or 1024)", h);
+  else if (h == 2048) R = 32;   // two 1024-point warp FFTs + a radix-2 step per line (pce2k.cu)
+  else return set_error(RK_ERR_UNSUPPORTED, "PCE pattern side %d not built (256, 1024 or 2048)", h);
   PceState& st = app->pce;
   st.R = R;
   st.N = h;
-  st.batch = app->p.batch_pairs > 0 ? app->p.batch_pairs : (R == 32 ? 16 : 64);
+  st.batch = app->p.batch_pairs > 0 ? app->p.batch_pairs : (h == 2048 ? 8 : R == 32 ? 16 : 64);
   if (st.batch > kMaxBatch) st.batch = kMaxBatch;
   const int N = st.N;
   app->slot_bytes = (size_t)N * N * sizeof(float);       // (N/2)*N complex64
@@ -706,13 +612,14 @@ rk_status pce_init(rk_app* app) {
   std::vector<float2> tw((size_t)R * R);
   for (int k1 = 0; k1 < R; ++k1)
     for (int n1 = 0; n1 < R; ++n1) {
-      const double ang = -2.0 * M_PI * (double)(n1 * k1) / (double)N;
+      const double ang = -2.0 * M_PI * (double)(n1 * k1) / (double)(R * R);
       tw[(size_t)k1 * R + n1] = make_float2((float)cos(ang), (float)sin(ang));
     }
   RK_CUDA(cudaMalloc(&st.tw, sizeof(float2) * R * R));
   RK_CUDA(cudaMemcpy(st.tw, tw.data(), sizeof(float2) * R * R, cudaMemcpyHostToDevice));
   RK_CUDA(cudaMalloc(&st.U, sizeof(float2) * (size_t)(N / 2) * N * st.batch));
   RK_CUDA(cudaMalloc(&st.mean_part, sizeof(float) * kMeanParts * st.batch));
+  if (N == 2048) return pce2k_init(app);
   if (R == 16) {
     RK_TRY(set_attrs<16>());
     return cluster_init<16>(app);
@@ -736,6 +643,8 @@ rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
   if (parsed_stride % 16 != 0) return set_error(RK_ERR_VALUE, "parsed_stride must be a multiple of 16 bytes");
   const float* pix = static_cast<const float*>(d_parsed);
   const size_t stride_f = parsed_stride / sizeof(float);
+  if (app->pce.N == 2048)
+    return pce2k_preprocess(app, pix, stride_f, n_items, static_cast<char*>(d_slots), slot_stride, h_slot_idx, s);
   if (app->pce.R == 16)
     return preprocess_impl<16>(app, pix, stride_f, n_items, static_cast<char*>(d_slots), slot_stride, h_slot_idx, s);
   return preprocess_impl<32>(app, pix, stride_f, n_items, static_cast<char*>(d_slots), slot_stride, h_slot_idx, s);

@@ -1,0 +1,117 @@
+// Device helpers shared by the PCE compare kernels (pce.cu: 256^2 / 1024^2,
+// pce2k.cu: 2048^2).  See pce.cu for the definitions of the score.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "fft.cuh"
+
+namespace rk {
+namespace pcek {
+
+constexpr int kWin = 11;                // PCE exclusion neighbourhood side
+constexpr int kHalfWin = kWin / 2;
+constexpr int kMeanParts = 64;          // CTAs per item in the mean reduction
+
+__device__ __forceinline__ bool better(float v, int idx, float bv, int bidx) {
+  return v > bv || (v == bv && idx < bidx);
+}
+
+// ---------------------------------------------------------------------------
+// T (the column pass output) layout per pair: blocks of 8 rows; block rb holds
+// all N/2 columns x 8 rows, the 8 rows of one column in 64 contiguous bytes
+// whose four 16-byte row-pair chunks are XOR-swizzled by ((column >> 1) & 3), so
+// eight consecutive columns of one row pair hit eight distinct bank groups.  A
+// column FFT stores four 64-B segments per warp instruction; an 8-row block is
+// one contiguous bulk copy (TMA) feeding four warps, one row pair each.
+template <int N>
+__device__ __forceinline__ size_t t_index8(int r, int c) {
+  const int rb = r >> 3, rr = r & 7;
+  const int pos = (((rr >> 1) ^ ((c >> 1) & 3)) << 1) | (rr & 1);
+  return ((size_t)rb * (N / 2) + c) * 8 + pos;
+}
+
+// Z[k] = A[k] + i*B[k] for row pair rp (rows 2rp, 2rp+1) of a staged 8-row block
+// ([c][8] with the chunk swizzle), Hermitian-extended; column 0 packs DC + i*Nyquist.
+template <int R>
+__device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk, int rp, int lane) {
+  constexpr int N = R * R;
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) {
+    const int k = lane + R * n2;
+    int kk = (n2 < R / 2) ? k : N - k;
+    if (kk >= N / 2) kk = 0;   // lane 0 at k = N/2: the Nyquist value lives in column 0
+    const float4 q = *reinterpret_cast<const float4*>(blk + kk * 8 + 2 * (rp ^ ((kk >> 1) & 3)));
+    float2 a = make_float2(q.x, q.y), c = make_float2(q.z, q.w);
+    if (n2 >= R / 2) {
+      a.y = -a.y;
+      c.y = -c.y;
+    }
+    if (kk == 0) {
+      a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
+      c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
+    }
+    v[n2] = make_float2(a.x - c.y, a.y + c.x);
+  }
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+struct ArgMax {
+  float v;
+  int idx;
+};
+
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, a.v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, a.idx, o);
+    if (better(ov, oi, a.v, a.idx)) {
+      a.v = ov;
+      a.idx = oi;
+    }
+  }
+  return a;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Running (max, first index, sum of squares) over one row pair of C.
+template <int R>
+__device__ __forceinline__ void argmax_update(const float2 (&v)[R], int ra, int lane, float& m, int& idx, float& ss) {
+  constexpr int N = R * R;
+  float lm = -INFINITY;
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) {
+    ss = fmaf(v[k2].x, v[k2].x, ss);
+    ss = fmaf(v[k2].y, v[k2].y, ss);
+    lm = fmaxf(lm, fmaxf(v[k2].x, v[k2].y));
+  }
+  if (lm >= m) {
+    int li = 0x7fffffff;
+#pragma unroll
+    for (int k2 = R - 1; k2 >= 0; --k2)
+      if (v[k2].x == lm) li = ra * N + lane + R * k2;
+    if (li == 0x7fffffff) {
+#pragma unroll
+      for (int k2 = R - 1; k2 >= 0; --k2)
+        if (v[k2].y == lm) li = (ra + 1) * N + lane + R * k2;
+    }
+    if (lm > m || li < idx) {
+      m = lm;
+      idx = li;
+    }
+  }
+}
+
+}  // namespace pcek
+}  // namespace rk

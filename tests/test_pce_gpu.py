@@ -30,8 +30,17 @@ def make_items(n, side, cameras=2, seed=11, first_key=0):
 
 
 def unpack_slot(slot_bytes: np.ndarray, n: int) -> np.ndarray:
-    """Device slot layout -> numpy rfft2 layout (n x (n/2+1))."""
-    z = slot_bytes.view(np.complex64).reshape(n // 2, n).astype(np.complex128)  # [col][row]
+    """Device slot layout -> numpy rfft2 layout (n x (n/2+1)).
+
+    256/1024: [col][row]; 2048: [row parity][col][row >> 1] (csrc/pce2k.cu header).
+    """
+    if n == 2048:
+        zp = slot_bytes.view(np.complex64).reshape(2, n // 2, n // 2).astype(np.complex128)
+        z = np.empty((n // 2, n), dtype=np.complex128)
+        z[:, 0::2] = zp[0]
+        z[:, 1::2] = zp[1]
+    else:
+        z = slot_bytes.view(np.complex64).reshape(n // 2, n).astype(np.complex128)  # [col][row]
     s = np.zeros((n, n // 2 + 1), dtype=np.complex128)
     s[:, 1:n // 2] = z[1:].T
     p = z[0]
@@ -41,7 +50,7 @@ def unpack_slot(slot_bytes: np.ndarray, n: int) -> np.ndarray:
     return s
 
 
-@pytest.mark.parametrize("side", [256, 1024])
+@pytest.mark.parametrize("side", [256, 1024, 2048])
 def test_preprocess_spectrum_layout(side):
     _l, device = _lib()
     n = 3
@@ -59,7 +68,7 @@ def test_preprocess_spectrum_layout(side):
         assert err < 1e-5, (side, k, err)   # fp32 FFT vs float64
 
 
-@pytest.mark.parametrize("side,n", [(256, 7), (1024, 4)])
+@pytest.mark.parametrize("side,n", [(256, 7), (1024, 4), (2048, 4)])
 def test_allpairs_matches_oracle(side, n):
     _l, device = _lib()
     items = make_items(n, side, cameras=2)
@@ -84,11 +93,14 @@ def test_allpairs_matches_oracle(side, n):
             assert (v > 60.0) == (i % 2 == j % 2), (i, j, v)
 
 
-def test_shifted_copy_peak():
+@pytest.mark.parametrize("side,shift", [(256, (5, -9)), (2048, (5, -9)), (2048, (0, 3)), (2048, (-1029, 1500)),
+                                        (1024, (1, -517))])
+def test_shifted_copy_peak(side, shift):
+    """Peak at the shift, including wrap-around windows (row 0 / last row block) and
+    peaks in the second half of a 2048 line (the radix-2 step's X[k + 1024] outputs)."""
     _l, device = _lib()
-    side = 256
     base = make_items(1, side, cameras=1, seed=3).view(side, side)
-    shifted = torch.roll(base, shifts=(5, -9), dims=(0, 1))
+    shifted = torch.roll(base, shifts=shift, dims=(0, 1))
     items = torch.stack([base, shifted]).contiguous().view(-1)
     app = device.DeviceApp(_l.app_params(_l.APP_PCE, 2, height=side, width=side))
     slots = app.alloc_slots(2)
@@ -99,7 +111,7 @@ def test_shifted_copy_peak():
     host = items.cpu().numpy().reshape(2, side, side)
     s0, s1 = opce.preprocess(host[0]), opce.preprocess(host[1])
     want, _, idx = opce.pce_from_plane(opce.correlation(s0, s1, side, side))
-    assert divmod(idx, side) == ((-5) % side, 9)
+    assert divmod(idx, side) == ((-shift[0]) % side, (-shift[1]) % side)
     assert out.item() == pytest.approx(want, rel=RTOL)
     assert out.item() > 1e4
 
@@ -148,3 +160,22 @@ def test_engine_host_items_matches_device_items():
         eng.run(out, parsed_stride=side * side * 4, **kw)
         outs.append(out.cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_engine_2048_with_evictions():
+    """C3 item shape through the engine with a slot tier smaller than n (reloads)."""
+    _l, device = _lib()
+    side, n = 2048, 5
+    items = make_items(n, side, cameras=2, seed=21)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side, threshold=60.0), leaf_block=2,
+                              device_slots=3)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+    want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
+    got = out.cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=RTOL)
+    assert np.array_equal(flags.cpu().numpy() == 3, got >= 60.0)
+    st = eng.stats()
+    assert st["pairs_done"] == total and st["evictions"] > 0
