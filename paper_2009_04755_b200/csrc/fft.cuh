@@ -359,4 +359,21 @@ __device__ __forceinline__ void group_fft_pad(float2 (&v)[R], float2* xbuf, cons
   dft_regs<R, INV>(v);
 }
 
+// group_fft_pad with the lane's twiddles W_N^(lane*k1) held in registers.
+template <int R, bool INV>
+__device__ __forceinline__ void group_fft_pad_rt(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
+  dft_regs<R, INV>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < R; ++k1) v[k1] = c_mul(v[k1], INV ? c_conj(w[k1]) : w[k1]);
+  float2* wr = xbuf + lane * (R + 1);
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) wr[k1] = v[k1];
+  __syncwarp();
+  const float2* rd = xbuf + lane;
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = rd[n1 * (R + 1)];
+  __syncwarp();
+  dft_regs<R, INV>(v);
+}
+
 }  // namespace rk

@@ -292,6 +292,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, c
   }
   uint32_t ph = 0, wph = 0;
   __syncthreads();
+  // hot-loop FFTs: lane twiddles in registers (default) or from the shared table
+#ifndef PCE2K_SMEM_TW
+  float2 twr[R];
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) twr[k1] = tw[k1 * R + lane];
+#define PCE2K_FFT(v) group_fft_pad_rt<R, true>(v, xbuf, twr, lane)
+#else
+#define PCE2K_FFT(v) group_fft_pad<R, true>(v, xbuf, tw, lane)
+#endif
   const float2 wl = lane_w2048(lane);
   const uint64_t pol = l2_policy_evict_normal();
   const uint64_t pol_first = l2_policy_evict_first();
@@ -354,9 +363,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, c
         const int col = 4 * (wg + 2 * (u >> 1)) + gi;
         float2 e[R], o[R];
         product(u, e);
-        group_fft_pad<R, true>(e, xbuf, tw, lane);
+        PCE2K_FFT(e);
         product(u + 1, o);
-        group_fft_pad<R, true>(o, xbuf, tw, lane);
+        PCE2K_FFT(o);
         radix2_last<true>(e, o, wl);
         // row n = lane + R*k1 -> block (lane >> 3) + 4*k1, row lane & 7; row n + H -> block + 128
         const int j = col >> 1;
@@ -397,13 +406,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, c
         block8_rows_z<R>(e, gb, gi, lane);
         named_bar(1 + wg, kGW * 32);
         if (leader && rb + 2 < kBlocks) issue(rb + 2, 0);
-        group_fft_pad<R, true>(e, xbuf, tw, lane);
+        PCE2K_FFT(e);
         mbar_wait(&s_bar[wg][2], (ph >> 2) & 1u);
         ph ^= 4u;
         half_rows_zodd(o, gb + kUnitF2, gi, lane);
         named_bar(1 + wg, kGW * 32);
         if (leader && rb + 2 < kBlocks) issue(rb + 2, 1);
-        group_fft_pad<R, true>(o, xbuf, tw, lane);
+        PCE2K_FFT(o);
         radix2_last<true>(e, o, wl);
         argmax2k_update(e, o, 8 * rb + 2 * gi, lane, m, idx, ss);
       }
