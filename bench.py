@@ -11,13 +11,16 @@ rank's share through the fused compare kernels.
           timed region, timed with CUDA events on the engine stream, max over ranks
   e2e     the same job through the public engine API from pinned HOST patterns,
           H2D inside the timed region, plus the D2H of the packed result triangle
-  roofline  dominant kernel = one PCE compare batch (pce_corr_cols + pce_rows_reduce)
+  roofline  dominant kernel = one PCE compare launch (pce_cluster; pce2k_pair at 2048^2),
+          per-launch time from sampled CUDA events on the engine stream
   cpu_baseline  the float64 oracle (oracle/pce.py) on a bounded pair sample
 
 `python bench.py --impl reference` times the reference-side CPU path (the
 oracle port; the reference itself has no PCE) on the same workload.
 Multi-GPU: launched under torchrun, leaves are sharded across ranks (strong
-scaling of one job); NCCL is used once, to reduce the result triangle to rank 0.
+scaling of one job); every item is preprocessed once on its home GPU (k mod N)
+and other ranks fetch it over NVLink (peer tier, CUDA IPC); NCCL is used once,
+to reduce the result triangle to rank 0.
 """
 
 from __future__ import annotations
@@ -181,7 +184,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n, side = args.n, args.side
     pairs_total = n * (n - 1) // 2
-    workload = f"PRNU PCE all-pairs, N={n} patterns of {side}x{side} fp32 (BASELINE configs[1])"
+    cfg_name = {(4096, 1024): " (BASELINE configs[1])", (16384, 2048): " (BASELINE configs[2])"}.get((n, side), "")
+    workload = f"PRNU PCE all-pairs, N={n} patterns of {side}x{side} fp32{cfg_name}"
     metric = "pairs/sec (whole box)"
 
     if args.impl == "reference":
@@ -360,6 +364,8 @@ def main():
         with open(os.path.join(ROOT, "profiles", "pce_cluster_traffic.json")) as fh:
             tj = json.load(fh)
         traffic_per_pair = (tj["dram_bytes_read_per_launch"] + tj["dram_bytes_write_per_launch"]) / tj["pairs_per_launch"]
+        if tj.get("side", 1024) != side:
+            traffic_per_pair = None      # the capture is for another pattern size
     except Exception:
         traffic_per_pair = None
     if ksamples:
@@ -371,7 +377,8 @@ def main():
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "traffic": traffic,
                     "traffic_source": "profiles/pce_cluster_traffic.json (ncu dram__bytes_read+write, per launch)",
-                    "kernel": "pce_cluster (persistent, one CTA = one SM per pair in flight: column + row pass)",
+                    "kernel": ("pce_cluster" if side <= 1024 else "pce2k_pair")
+                              + " (persistent, one CTA = one SM per pair in flight: column + row pass)",
                     "pairs_per_launch": batch, "ms_per_launch": per_launch_ms,
                     "alg_bytes_per_pair": alg_bytes_per_pair, "peak_source": peaks_src,
                     "fp32_flops_per_pair": 2 * 5 * (side // 2) * side * math.log2(side)}
@@ -384,7 +391,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
             "config": {"workload": workload, "n": n, "side": side, "pairs": pairs_total, "leaf_block": args.leaf,
-                       "parallelism": f"pairs{world}", "l2": "inputs (16 GiB patterns + 16 GiB spectra) >> L2"},
+                       "parallelism": f"pairs{world}", "l2": f"inputs ({2 * n * slot_bytes / 2**30:.0f} GiB patterns + spectra) >> L2 (126 MB)"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": st["kernel_launches"],
             "cache": {"R": loads_all / n, "loads_per_step": loads_all,
