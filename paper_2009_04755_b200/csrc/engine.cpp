@@ -148,7 +148,16 @@ struct rk_engine {
   rk_engine_params p{};
   int device = 0;
   rk_app* app = nullptr;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;    // compare stream (rk_engine_stream)
+  // Load pipeline (engine.py:436-487 on a stream of its own): H2D + preprocess and
+  // peer fetches of the next leaves run on `lstream` while the compare stream
+  // executes the current batch.  Ordering: a compare batch waits for `ev_loaded`
+  // (the last load issued before it); a load into an evicted slot waits for
+  // `ev_compared` (every compare launched before the eviction).
+  cudaStream_t lstream = nullptr;
+  cudaEvent_t ev_loaded = nullptr;
+  cudaEvent_t ev_compared = nullptr;
+  bool loads_unsynced = false;      // loads issued since the compare stream last waited
   void* arena = nullptr;
   size_t slot_stride = 0;
   void* staging = nullptr;
@@ -179,6 +188,10 @@ struct LoadReq {
 
 rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, uint8_t* d_flags) {
   if (pend.empty()) return RK_OK;
+  if (e->loads_unsynced) {   // the batch reads slots loaded on the load stream
+    RK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_loaded, 0));
+    e->loads_unsynced = false;
+  }
   const int lim = batch_limit(e->app);
   for (size_t base = 0; base < pend.size(); base += lim) {
     const int m = (int)std::min<size_t>(lim, pend.size() - base);
@@ -210,10 +223,10 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
       for (int k = 0; k < m; ++k) {
         const char* src = static_cast<const char*>(h_parsed) + (size_t)loads[base + k].key * parsed_stride;
         RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->staging) + (size_t)k * pbytes, src, pbytes,
-                                cudaMemcpyHostToDevice, e->stream));
+                                cudaMemcpyHostToDevice, e->lstream));
         e->stats.h2d_bytes += (int64_t)pbytes;
       }
-      RK_TRY(rk_preprocess(e->app, e->staging, pbytes, m, e->arena, e->slot_stride, slots.data(), e->stream));
+      RK_TRY(rk_preprocess(e->app, e->staging, pbytes, m, e->arena, e->slot_stride, slots.data(), e->lstream));
     } else {
       // device-resident parsed items: preprocess runs of consecutive keys in place
       int k = 0;
@@ -221,7 +234,7 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
         int run = 1;
         while (k + run < m && loads[base + k + run].key == loads[base + k].key + run) ++run;
         const char* src = static_cast<const char*>(d_parsed) + (size_t)loads[base + k].key * parsed_stride;
-        RK_TRY(rk_preprocess(e->app, src, parsed_stride, run, e->arena, e->slot_stride, slots.data() + k, e->stream));
+        RK_TRY(rk_preprocess(e->app, src, parsed_stride, run, e->arena, e->slot_stride, slots.data() + k, e->lstream));
         k += run;
       }
     }
@@ -229,6 +242,8 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
   }
   for (const LoadReq& l : loads) e->tier->publish(l.slot, true);  // retained lease (slotcache.py:188-213)
   loads.clear();
+  RK_CUDA(cudaEventRecord(e->ev_loaded, e->lstream));
+  e->loads_unsynced = true;
   return RK_OK;
 }
 
@@ -261,6 +276,11 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   e->slot_stride = (e->app->slot_bytes + 255) / 256 * 256;
   cudaError_t ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaStreamCreate"));
+  ce = cudaStreamCreateWithFlags(&e->lstream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaStreamCreate(load)"));
+  ce = cudaEventCreateWithFlags(&e->ev_loaded, cudaEventDisableTiming);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_compared, cudaEventDisableTiming);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaEventCreate"));
   if (params->peer_tier && params->world > 1)
     e->home_slots = (app_params->n + params->world - 1) / params->world;
   ce = cudaMalloc(&e->arena, e->slot_stride * ((size_t)params->device_slots + e->home_slots));
@@ -279,6 +299,9 @@ void rk_engine_destroy(rk_engine* e) {
   cudaSetDevice(e->device);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->lstream) cudaStreamDestroy(e->lstream);
+  if (e->ev_loaded) cudaEventDestroy(e->ev_loaded);
+  if (e->ev_compared) cudaEventDestroy(e->ev_compared);
   cudaFree(e->arena);
   cudaFree(e->staging);
   delete e->tier;
@@ -318,6 +341,10 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->tier->evictions = ev;
   }
   const int64_t launches0 = e->app->launches;
+  // the load stream starts after everything already queued on the engine stream
+  RK_CUDA(cudaEventRecord(e->ev_compared, e->stream));
+  RK_CUDA(cudaStreamWaitEvent(e->lstream, e->ev_compared, 0));
+  e->loads_unsynced = false;
   if (e->app->p.kind == RK_APP_NCC) {
     // Gram path: every item resident in slot == key, then one tcgen05 GEMM over
     // this rank's upper-triangle tiles
@@ -330,6 +357,8 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     }
     RK_TRY(flush_loads(e, all, h_parsed, d_parsed, parsed_stride));
     for (int32_t k = 0; k < n; ++k) e->tier->release(e->tier->find(k));
+    if (e->loads_unsynced) RK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_loaded, 0));
+    e->loads_unsynced = false;
     RK_TRY(rk_ncc_gram(e->app, e->arena, e->slot_stride, e->tier->capacity, e->p.rank, e->p.world, d_out, d_flags,
                        e->stream));
     const int side = (n + 127) / 128;
@@ -389,8 +418,13 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
                          keys.size());
       }
       if (r.kind == kMiss) {
-        // the victim may still be read by pairs not yet launched
-        if (e->tier->evictions != evictions_before) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+        // the victim may still be read by pairs not yet launched, or launched and
+        // still running on the compare stream: the load into it waits for them
+        if (e->tier->evictions != evictions_before) {
+          RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+          RK_CUDA(cudaEventRecord(e->ev_compared, e->stream));
+          RK_CUDA(cudaStreamWaitEvent(e->lstream, e->ev_compared, 0));
+        }
         if (peer) fetches.push_back(LoadReq{k, r.slot});
         else loads.push_back(LoadReq{k, r.slot});
       }
@@ -404,12 +438,14 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
       for (const LoadReq& f : fetches) {
         const char* src = e->peer_home[f.key % world] + (size_t)(f.key / world) * e->slot_stride;
         char* dst = static_cast<char*>(e->arena) + (size_t)f.slot * e->slot_stride;
-        RK_CUDA(cudaMemcpyAsync(dst, src, sb, cudaMemcpyDeviceToDevice, e->stream));
+        RK_CUDA(cudaMemcpyAsync(dst, src, sb, cudaMemcpyDeviceToDevice, e->lstream));
         e->tier->publish(f.slot, true);
         e->stats.peer_fetches += 1;
         e->stats.peer_bytes += (int64_t)sb;
       }
       fetches.clear();
+      RK_CUDA(cudaEventRecord(e->ev_loaded, e->lstream));
+      e->loads_unsynced = true;
     }
     for (int32_t i = l.r0; i < l.r1; ++i)
       for (int32_t j = std::max(l.c0, i + 1); j < l.c1; ++j) {
@@ -420,6 +456,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   }
   RK_TRY(flush_pairs(e, pend, d_out, d_flags));
   (void)world;
+  RK_CUDA(cudaStreamSynchronize(e->lstream));
   RK_CUDA(cudaStreamSynchronize(e->stream));
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;

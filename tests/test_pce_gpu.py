@@ -147,7 +147,10 @@ def test_engine_matches_oracle(device_slots, leaf):
         assert st["loads"] > n and st["evictions"] > 0
 
 
-def test_engine_host_items_matches_device_items():
+@pytest.mark.parametrize("device_slots", [None, 5])
+def test_engine_host_items_matches_device_items(device_slots):
+    """Host (H2D on the load stream) and device inputs agree bit-for-bit, also when
+    loads into evicted slots must wait for the compares still reading them."""
     _l, device = _lib()
     side, n = 256, 9
     items = make_items(n, side, cameras=2, seed=9)
@@ -155,7 +158,8 @@ def test_engine_host_items_matches_device_items():
     total = n * (n - 1) // 2
     outs = []
     for kw in ({"device_items": items}, {"host_items": host}):
-        eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=4)
+        eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=4,
+                                  **({} if device_slots is None else {"device_slots": device_slots}))
         out = torch.zeros(total, dtype=torch.float64, device="cuda")
         eng.run(out, parsed_stride=side * side * 4, **kw)
         outs.append(out.cpu().numpy())
