@@ -54,6 +54,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-steal", action="store_true", help="N > 1: static leaf shares, no cross-GPU stealing")
     return ap.parse_args()
 
 
@@ -228,8 +229,10 @@ def main():
     # N > 1: peer-GPU tier -- each rank preprocesses its home items (k % N == rank),
     # every other item it needs is copied from its home GPU over NVLink (CUDA IPC)
     peer = world > 1
+    # and ranks take leaf chunks from device work-queue words, stealing across GPUs
+    steal = peer and not args.no_steal
     eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=n, rank=rank, world=world,
-                              device=local_rank, peer_tier=peer)
+                              device=local_rank, peer_tier=peer, steal=steal)
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
@@ -254,6 +257,8 @@ def main():
             if not state["connected"]:
                 eng.connect_peers()
                 state["connected"] = True
+            if steal:
+                eng.queue_reset()
             barrier()
             eng.run(out, flags, host_items=host_home, device_items=None if host_home is not None else items,
                     parsed_stride=parsed_bytes)
@@ -299,11 +304,11 @@ def main():
     value = all_pairs / (ms / 1e3)
     eng.set_profiling(0)
     # cache accounting over the whole job (runner.py:41 R = loads / n; slotcache.py:252-260 tiers)
-    ct = torch.tensor([st["loads"], st["hits"], st["misses"], st["peer_fetches"]], dtype=torch.float64,
-                      device="cuda")
+    ct = torch.tensor([st["loads"], st["hits"], st["misses"], st["peer_fetches"], st["steals"]],
+                      dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ct, op=dist.ReduceOp.SUM)
-    loads_all, hits_all, misses_all, peer_all = [float(x) / max(1, args.steps) for x in ct.tolist()]
+    loads_all, hits_all, misses_all, peer_all, steals_all = [float(x) / max(1, args.steps) for x in ct.tolist()]
 
     # ---- e2e: pinned host patterns -> engine -> packed triangle back on host
     e2e = None
@@ -398,7 +403,8 @@ def main():
                       "device_hit_rate": hits_all / max(1.0, hits_all + misses_all),
                       "device_hits_per_step": hits_all, "device_misses_per_step": misses_all,
                       "peer_fetches_per_step": peer_all,
-                      "peer_hit_rate": peer_all / max(1.0, misses_all) if world > 1 else None}}
+                      "peer_hit_rate": peer_all / max(1.0, misses_all) if world > 1 else None,
+                      "steals_per_step": steals_all if world > 1 else None}}
     print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     eng.close()

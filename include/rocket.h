@@ -147,6 +147,8 @@ typedef struct {
   int32_t rank;            /* this rank's share of the leaves ... */
   int32_t world;           /* ... out of world (contiguous, pair-balanced DFS blocks of leaves) */
   int32_t peer_tier;       /* world > 1: items live on their home GPU (k mod world), others fetch them over NVLink */
+  int32_t steal;           /* world > 1: dynamic leaf chunks + cross-GPU stealing through device atomics */
+  int32_t steal_chunk;     /* leaves per grab (0: one compare batch worth) */
 } rk_engine_params;
 
 typedef struct {
@@ -161,6 +163,7 @@ typedef struct {
   int64_t kernel_launches;
   int64_t peer_fetches;    /* items copied from a peer GPU's home region (the remote tier, distcache.py) */
   int64_t peer_bytes;
+  int64_t steals;          /* chunks this rank stole from other ranks' queues */
 } rk_engine_stats;
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,
@@ -188,6 +191,18 @@ rk_status rk_engine_arena(const rk_engine* eng, void** d_base, size_t* slot_stri
 rk_status rk_engine_load_home(rk_engine* eng, const void* h_parsed, const void* d_parsed, size_t parsed_stride);
 rk_status rk_engine_set_peer_homes(rk_engine* eng, int32_t world, void* const* d_home_bases);
 /* CUDA IPC of a device allocation (64-byte handle) for the peer tier. */
+/* Cross-GPU work queue (hierarchical stealing, engine.py:274-309 and
+ * scheduler.py:126-157 for the GPUs of one box).  Each rank's 64-bit queue word
+ * (head << 32 | tail over the global depth-first leaf list) lives in device
+ * memory at the tail of its slot arena (rk_engine_arena's allocation, so the
+ * home-region IPC handle maps it too).  Before every run with steal != 0:
+ * rk_engine_queue_reset on every rank (own word <- its contiguous share), a
+ * barrier, then rk_engine_run.  rk_engine_set_peer_queues takes every rank's
+ * mapped word (own entry = local) once after the IPC exchange. */
+rk_status rk_engine_queue_word(const rk_engine* eng, void** d_word);
+rk_status rk_engine_queue_reset(rk_engine* eng);
+rk_status rk_engine_set_peer_queues(rk_engine* eng, int32_t world, void* const* d_words);
+
 rk_status rk_ipc_handle(const void* d_ptr, uint8_t* out_handle64);
 rk_status rk_ipc_open(const uint8_t* handle64, int device, void** d_ptr);
 rk_status rk_ipc_close(void* d_ptr);

@@ -59,6 +59,8 @@ class EngineParams(C.Structure):
         ("rank", C.c_int32),
         ("world", C.c_int32),
         ("peer_tier", C.c_int32),
+        ("steal", C.c_int32),
+        ("steal_chunk", C.c_int32),
     ]
 
 
@@ -75,6 +77,7 @@ class EngineStats(C.Structure):
         ("kernel_launches", C.c_int64),
         ("peer_fetches", C.c_int64),
         ("peer_bytes", C.c_int64),
+        ("steals", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -116,6 +119,9 @@ SIGNATURES = [
     ("rk_engine_arena", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     ("rk_engine_load_home", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     ("rk_engine_set_peer_homes", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rk_engine_queue_word", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("rk_engine_queue_reset", C.c_int, [C.c_void_p]),
+    ("rk_engine_set_peer_queues", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("rk_ipc_handle", C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     ("rk_ipc_open", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)]),
     ("rk_ipc_close", C.c_int, [C.c_void_p]),

@@ -69,6 +69,80 @@ std::vector<Leaf> rank_share(const std::vector<Leaf>& leaves, int rank, int worl
   return mine;
 }
 
+// The same share as an index range [lo, hi) of the DFS leaf list (owners are
+// non-decreasing along the list, so every share is contiguous).
+std::pair<int, int> rank_range(const std::vector<Leaf>& leaves, int rank, int world) {
+  if (world <= 1) return {0, (int)leaves.size()};
+  int64_t total = 0;
+  for (const Leaf& l : leaves) total += region_pairs(l.r0, l.r1, l.c0, l.c1);
+  int lo = -1, hi = -1;
+  int64_t prefix = 0;
+  for (int q = 0; q < (int)leaves.size(); ++q) {
+    const Leaf& l = leaves[q];
+    const int64_t pc = region_pairs(l.r0, l.r1, l.c0, l.c1);
+    const int owner = (int)std::min<int64_t>(world - 1, ((prefix + pc / 2) * world) / std::max<int64_t>(total, 1));
+    if (owner == rank) {
+      if (lo < 0) lo = q;
+      hi = q + 1;
+    }
+    prefix += pc;
+  }
+  if (lo < 0) return {0, 0};
+  return {lo, hi};
+}
+
+// ---------------------------------------------------------------------------
+// Cross-GPU work queue (hierarchical stealing, engine.py:274-309 and
+// scheduler.py:126-157 restated for one box): every rank owns a 64-bit word
+// (head << 32 | tail) over the global DFS leaf list, initialised to its
+// rank_range.  The owner takes chunks from the head (depth-first order, the
+// reference's pop at the back of its deque); a thief CASes away the back half of
+// the victim with the most remaining leaves (the largest task, like stealing at
+// the front) and publishes it as its own range, so it can be re-stolen.  The
+// words live in device memory and peers update them with system-scope atomics
+// over NVLink (CUDA IPC mappings); the host reads the result from mapped memory.
+__global__ void queue_op_kernel(unsigned long long* word, int op, unsigned long long arg,
+                                unsigned long long* res) {
+  unsigned long long old = atomicAdd_system(word, 0ull);
+  if (op == 2) {            // read
+    *res = old;
+    return;
+  }
+  if (op == 3) {            // set (own word, when it is empty or at reset)
+    atomicExch_system(word, arg);
+    *res = arg;
+    return;
+  }
+  for (;;) {
+    const unsigned h = (unsigned)(old >> 32), t = (unsigned)old;
+    const unsigned rem = t > h ? t - h : 0u;
+    unsigned long long nw, got;
+    if (op == 0) {          // owner: up to `arg` leaves from the head
+      if (rem == 0) {
+        *res = ~0ull;
+        return;
+      }
+      const unsigned take = rem < arg ? rem : (unsigned)arg;
+      nw = ((unsigned long long)(h + take) << 32) | t;
+      got = ((unsigned long long)h << 32) | (h + take);
+    } else {                // thief: the back half, if at least `arg` leaves remain on each side
+      if (rem < 2 * arg) {
+        *res = ~0ull;
+        return;
+      }
+      const unsigned k = rem / 2;
+      nw = ((unsigned long long)h << 32) | (t - k);
+      got = ((unsigned long long)(t - k) << 32) | t;
+    }
+    const unsigned long long prev = atomicCAS_system(word, old, nw);
+    if (prev == old) {
+      *res = got;
+      return;
+    }
+    old = prev;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Slot tier (CacheTier restated, slotcache.py:139-282)
 SlotTier::SlotTier(int cap) : capacity(cap) {
@@ -158,6 +232,15 @@ struct rk_engine {
   cudaEvent_t ev_loaded = nullptr;
   cudaEvent_t ev_compared = nullptr;
   bool loads_unsynced = false;      // loads issued since the compare stream last waited
+  // cross-GPU work queue (queue_op_kernel): own word at the arena's tail, peers' via IPC
+  unsigned long long* qword = nullptr;
+  std::vector<unsigned long long*> peer_q;
+  bool queues_ready = false;
+  cudaStream_t cstream = nullptr;   // control stream for the queue operations
+  unsigned long long* h_qres = nullptr;   // mapped pinned result word
+  unsigned long long* d_qres = nullptr;
+  cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+  int64_t steals = 0;
   void* arena = nullptr;
   size_t slot_stride = 0;
   void* staging = nullptr;
@@ -185,6 +268,15 @@ struct LoadReq {
   int32_t key;
   int32_t slot;
 };
+
+// One queue operation on `word` (own or a peer's), synchronous.
+rk_status queue_call(rk_engine* e, unsigned long long* word, int op, unsigned long long arg, unsigned long long* res) {
+  queue_op_kernel<<<1, 1, 0, e->cstream>>>(word, op, arg, e->d_qres);
+  RK_CUDA(cudaGetLastError());
+  RK_CUDA(cudaStreamSynchronize(e->cstream));
+  *res = *(volatile unsigned long long*)e->h_qres;
+  return RK_OK;
+}
 
 rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, uint8_t* d_flags) {
   if (pend.empty()) return RK_OK;
@@ -283,8 +375,17 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaEventCreate"));
   if (params->peer_tier && params->world > 1)
     e->home_slots = (app_params->n + params->world - 1) / params->world;
-  ce = cudaMalloc(&e->arena, e->slot_stride * ((size_t)params->device_slots + e->home_slots));
+  const size_t arena_bytes = e->slot_stride * ((size_t)params->device_slots + e->home_slots);
+  ce = cudaMalloc(&e->arena, arena_bytes + 256);   // + the work-queue word (shared with the home region over IPC)
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(slot arena)"));
+  e->qword = reinterpret_cast<unsigned long long*>(static_cast<char*>(e->arena) + arena_bytes);
+  ce = cudaMemset(e->qword, 0, 256);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaHostAlloc(&e->h_qres, 64, cudaHostAllocMapped);
+  if (ce == cudaSuccess) ce = cudaHostGetDevicePointer(&e->d_qres, e->h_qres, 0);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_chunk[0], cudaEventDisableTiming);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_chunk[1], cudaEventDisableTiming);
+  if (ce != cudaSuccess) return fail(check_cuda(ce, "work queue setup"));
   e->staging_items = std::max(1, batch_limit(e->app));
   if (e->app->p.kind == RK_APP_PCE) e->staging_items = e->app->pce.batch;
   ce = cudaMalloc(&e->staging, std::max<size_t>(e->app->parsed_bytes, 16) * e->staging_items);
@@ -302,6 +403,10 @@ void rk_engine_destroy(rk_engine* e) {
   if (e->lstream) cudaStreamDestroy(e->lstream);
   if (e->ev_loaded) cudaEventDestroy(e->ev_loaded);
   if (e->ev_compared) cudaEventDestroy(e->ev_compared);
+  for (cudaEvent_t ev : e->ev_chunk)
+    if (ev) cudaEventDestroy(ev);
+  if (e->cstream) cudaStreamDestroy(e->cstream);
+  if (e->h_qres) cudaFreeHost(e->h_qres);
   cudaFree(e->arena);
   cudaFree(e->staging);
   delete e->tier;
@@ -376,7 +481,10 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->stats.kernel_launches += e->app->launches - launches0;
     return RK_OK;
   }
-  const std::vector<Leaf> leaves = rank_share(quadtree_leaves(n, e->p.leaf_block), e->p.rank, e->p.world);
+  const std::vector<Leaf> all_leaves = quadtree_leaves(n, e->p.leaf_block);
+  const bool steal = e->p.steal && e->p.world > 1;
+  if (steal && !e->queues_ready)
+    return set_error(RK_ERR_VALUE, "work stealing: call rk_engine_queue_reset and rk_engine_set_peer_queues first");
   const bool peer = e->home_slots > 0;
   if (peer && !e->peers_ready)
     return set_error(RK_ERR_VALUE, "peer tier: call rk_engine_load_home and rk_engine_set_peer_homes first");
@@ -388,13 +496,13 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   std::vector<int32_t> pinned;
   std::vector<int32_t> slot_of(peer ? n : 0, -1);
   const int lim = batch_limit(e->app);
-  for (const Leaf& l : leaves) {
+  auto do_leaf = [&](const Leaf& l) -> rk_status {
     if (e->app->p.kind == RK_APP_SYNTHETIC) {
       // no item state: the hash needs only the keys (apps.py:201-208)
       RK_TRY(rk_compare_tile(e->app, nullptr, 0, l.r0, l.r1, l.c0, l.c1, nullptr, d_out, d_flags, e->stream));
       e->stats.pairs_done += region_pairs(l.r0, l.r1, l.c0, l.c1);
       e->stats.tiles += 1;
-      continue;
+      return RK_OK;
     }
     // ascending key acquisition over the leaf's items (engine.py:510-516)
     keys.clear();
@@ -453,11 +561,59 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
         if ((int)pend.size() >= lim) RK_TRY(flush_pairs(e, pend, d_out, d_flags));
       }
     for (int s : pinned) e->tier->release(s);
+      return RK_OK;
+  };
+  if (!steal) {
+    const auto rr = rank_range(all_leaves, e->p.rank, e->p.world);
+    for (int q = rr.first; q < rr.second; ++q) RK_TRY(do_leaf(all_leaves[q]));
+  } else {
+    // dynamic: chunks from the own queue word, then steals; at most two chunks in
+    // flight on the GPU so grabbing stays close to execution (balance at the tail)
+    const int leaf_pairs = std::max(1, e->p.leaf_block * e->p.leaf_block);
+    const unsigned long long chunk =
+        e->p.steal_chunk > 0 ? (unsigned long long)e->p.steal_chunk : (unsigned long long)std::max(1, lim / leaf_pairs);
+    int64_t c = 0;
+    for (;;) {
+      unsigned long long got = ~0ull;
+      if (c >= 2) RK_CUDA(cudaEventSynchronize(e->ev_chunk[c & 1]));   // chunk c - 2 finished
+      RK_TRY(queue_call(e, e->qword, 0, chunk, &got));
+      while (got == ~0ull) {
+        // own range exhausted: steal from the rank with the most remaining leaves
+        int best = -1;
+        unsigned best_rem = 0;
+        for (int v = 0; v < world; ++v) {
+          if (v == e->p.rank) continue;
+          unsigned long long w = 0;
+          RK_TRY(queue_call(e, e->peer_q[v], 2, 0, &w));
+          const unsigned h = (unsigned)(w >> 32), t = (unsigned)w;
+          const unsigned rem = t > h ? t - h : 0u;
+          if (rem >= 2 * chunk && rem > best_rem) {
+            best = v;
+            best_rem = rem;
+          }
+        }
+        if (best < 0) break;
+        unsigned long long st = ~0ull;
+        RK_TRY(queue_call(e, e->peer_q[best], 1, chunk, &st));
+        if (st == ~0ull) continue;   // lost the race: look again
+        e->steals += 1;
+        unsigned long long tmp = 0;
+        RK_TRY(queue_call(e, e->qword, 3, st, &tmp));   // the stolen range is now ours (and stealable)
+        RK_TRY(queue_call(e, e->qword, 0, chunk, &got));
+      }
+      if (got == ~0ull) break;
+      const int a = (int)(got >> 32), b = (int)(unsigned)got;
+      for (int q = a; q < b; ++q) RK_TRY(do_leaf(all_leaves[q]));
+      RK_TRY(flush_pairs(e, pend, d_out, d_flags));
+      RK_CUDA(cudaEventRecord(e->ev_chunk[c & 1], e->stream));
+      ++c;
+    }
   }
   RK_TRY(flush_pairs(e, pend, d_out, d_flags));
   (void)world;
   RK_CUDA(cudaStreamSynchronize(e->lstream));
   RK_CUDA(cudaStreamSynchronize(e->stream));
+  e->stats.steals = e->steals;
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;
   e->stats.evictions = e->tier->evictions;
@@ -474,6 +630,7 @@ rk_status rk_engine_stats_get(const rk_engine* e, rk_engine_stats* out) {
 rk_status rk_engine_reset_stats(rk_engine* e) {
   if (!e) return set_error(RK_ERR_VALUE, "null engine");
   e->stats = rk_engine_stats{};
+  e->steals = 0;
   e->tier->hits = e->tier->misses = e->tier->waits = e->tier->evictions = 0;
   return RK_OK;
 }
@@ -545,6 +702,29 @@ rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_
     e->stats.loads += m;
   }
   RK_CUDA(cudaStreamSynchronize(e->stream));
+  return RK_OK;
+}
+
+rk_status rk_engine_queue_word(const rk_engine* e, void** d_word) {
+  if (!e || !d_word) return set_error(RK_ERR_VALUE, "null argument");
+  *d_word = e->qword;
+  return RK_OK;
+}
+
+rk_status rk_engine_queue_reset(rk_engine* e) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  RK_CUDA(cudaSetDevice(e->device));
+  const auto rr = rank_range(quadtree_leaves(e->app->p.n, e->p.leaf_block), e->p.rank, e->p.world);
+  unsigned long long tmp = 0;
+  return queue_call(e, e->qword, 3, ((unsigned long long)rr.first << 32) | (unsigned)rr.second, &tmp);
+}
+
+rk_status rk_engine_set_peer_queues(rk_engine* e, int32_t world, void* const* d_words) {
+  if (!e || !d_words) return set_error(RK_ERR_VALUE, "null argument");
+  if (world != e->p.world) return set_error(RK_ERR_VALUE, "work queue world mismatch");
+  e->peer_q.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) e->peer_q[r] = static_cast<unsigned long long*>(d_words[r]);
+  e->queues_ready = true;
   return RK_OK;
 }
 

@@ -87,12 +87,14 @@ class DeviceEngine:
     """rk_engine: quadtree tiles over an HBM slot tier, fed by host or device items."""
 
     def __init__(self, params: _lib.AppParams, *, leaf_block: int = 8, device_slots: int = 0,
-                 rank: int = 0, world: int = 1, device: int = 0, peer_tier: bool = False):
+                 rank: int = 0, world: int = 1, device: int = 0, peer_tier: bool = False, steal: bool = False,
+                 steal_chunk: int = 0):
         self.params = params
         self.device = device
         self.rank, self.world = rank, world
         slots = device_slots if device_slots > 0 else max(2, params.n)
-        ep = _lib.EngineParams(leaf_block, slots, 1, rank, world, int(bool(peer_tier and world > 1)))
+        ep = _lib.EngineParams(leaf_block, slots, 1, rank, world, int(bool(peer_tier and world > 1)),
+                               int(bool(steal and world > 1)), steal_chunk)
         handle = C.c_void_p()
         check(lib.rk_engine_create(C.byref(params), C.byref(ep), device, C.byref(handle)))
         self.handle = handle
@@ -150,29 +152,48 @@ class DeviceEngine:
         torch.cuda.current_stream(self.device).synchronize()
         check(lib.rk_engine_load_home(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride))
 
+    @property
+    def steal(self) -> bool:
+        return bool(self.engine_params.steal)
+
     def connect_peers(self) -> None:
-        """Exchange home regions over CUDA IPC (handles travel through torch.distributed)."""
+        """Map every rank's slot arena over CUDA IPC (handles travel through
+        torch.distributed): the home regions (peer tier) and the work-queue words
+        (stealing) are offsets into it."""
         import torch.distributed as dist
         base, nbytes = C.c_void_p(), C.c_size_t()
         check(lib.rk_engine_home_region(self.handle, C.byref(base), C.byref(nbytes)))
         arena, stride = C.c_void_p(), C.c_size_t()
         check(lib.rk_engine_arena(self.handle, C.byref(arena), C.byref(stride)))
+        qword = C.c_void_p()
+        check(lib.rk_engine_queue_word(self.handle, C.byref(qword)))
         hbuf = (C.c_uint8 * 64)()
         check(lib.rk_ipc_handle(arena, hbuf))
-        mine = (bytes(hbuf), int(base.value) - int(arena.value))
+        a0 = int(arena.value)
+        mine = (bytes(hbuf), int(base.value or a0) - a0, int(qword.value) - a0)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
-        ptrs = (C.c_void_p * self.world)()
+        homes = (C.c_void_p * self.world)()
+        queues = (C.c_void_p * self.world)()
         self._opened = []
-        for r, (h, off) in enumerate(everyone):
+        for r, (h, hoff, qoff) in enumerate(everyone):
             if r == self.rank:
-                ptrs[r] = base.value
-                continue
-            peer = C.c_void_p()
-            check(lib.rk_ipc_open((C.c_uint8 * 64)(*h), self.device, C.byref(peer)))
-            self._opened.append(peer)
-            ptrs[r] = peer.value + off
-        check(lib.rk_engine_set_peer_homes(self.handle, self.world, ptrs))
+                pbase = a0
+            else:
+                peer = C.c_void_p()
+                check(lib.rk_ipc_open((C.c_uint8 * 64)(*h), self.device, C.byref(peer)))
+                self._opened.append(peer)
+                pbase = int(peer.value)
+            homes[r] = pbase + hoff
+            queues[r] = pbase + qoff
+        if self.peer_tier:
+            check(lib.rk_engine_set_peer_homes(self.handle, self.world, homes))
+        if self.steal:
+            check(lib.rk_engine_set_peer_queues(self.handle, self.world, queues))
+
+    def queue_reset(self) -> None:
+        """Own work-queue word <- this rank's share; every rank, then a barrier, before run()."""
+        check(lib.rk_engine_queue_reset(self.handle))
 
     def close_peers(self) -> None:
         for p in getattr(self, "_opened", []):

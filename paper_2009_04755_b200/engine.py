@@ -8,10 +8,14 @@ slot tier (slotcache.py:159-282), loaded on a miss from the pinned host tier
 app's fused kernels.  Results land in the packed upper triangle indexed by
 PairLedger.pair_id (scheduler.py:228-231).
 
-Multi-GPU: one process per GPU (torchrun).  Each rank runs a contiguous,
-pair-balanced block of the depth-first leaves (no data-path communication);
-the disjoint result triangles are combined on rank 0 with one NCCL reduce --
-the only collective, as in the reference's completion gather to node 0
+Multi-GPU: one process per GPU (torchrun).  Each rank starts on a contiguous,
+pair-balanced block of the depth-first leaves and takes it in chunks from a
+work-queue word in its device memory; a rank that runs dry steals the back
+half of the fullest peer's remaining range with system-scope atomics over
+NVLink (hierarchical stealing, engine.py:274-309).  Items live on their home
+GPU (k mod world) and are fetched peer-to-peer (peer tier).  The disjoint
+result triangles are combined on rank 0 with one NCCL reduce -- the only
+collective, as in the reference's completion gather to node 0
 (engine.py:550-577).
 """
 
@@ -99,7 +103,8 @@ class AllPairsEngine:
     """All pairs of ``app``'s items on one GPU (this rank's share of a multi-GPU job)."""
 
     def __init__(self, app: B200Application, *, leaf_block: int = 16, device_slots: Optional[int] = None,
-                 rank: int = 0, world: int = 1, peer_tier: bool = True):
+                 rank: int = 0, world: int = 1, peer_tier: bool = True, steal: bool = True,
+                 steal_chunk: int = 0):
         self.app = app
         self.rank = rank
         self.world = world
@@ -107,7 +112,8 @@ class AllPairsEngine:
         slots = device_slots if device_slots is not None else app.n
         self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
                                  rank=rank, world=world, device=app.device,
-                                 peer_tier=peer_tier and world > 1 and app.kind not in (0, 3))
+                                 peer_tier=peer_tier and world > 1 and app.kind not in (0, 3),
+                                 steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk)
         self._peers_connected = False
         self._out = torch.empty(app.n * (app.n - 1) // 2, dtype=torch.float64, device=f"cuda:{app.device}")
         self._flags = torch.empty_like(self._out, dtype=torch.uint8)
@@ -135,9 +141,9 @@ class AllPairsEngine:
         self._eng.reset_stats()
         t0 = time.perf_counter()
         stride = self.app.parsed_bytes()
+        shared = self._eng.peer_tier or self._eng.steal
         if self._eng.peer_tier:
             # home items first (k % world == rank), then the IPC-mapped peer homes
-            import torch.distributed as dist
             # home item m = key rank + m*world: a strided view of the full item array
             off = self.rank * stride
 
@@ -151,15 +157,18 @@ class AllPairsEngine:
             self._eng.load_home(host_items=None if host_items is None else _At(host_items),
                                 device_items=None if device_items is None else _At(device_items),
                                 parsed_stride=self.world * stride)
+        if shared:
+            import torch.distributed as dist
             if not self._peers_connected:
                 self._eng.connect_peers()
                 self._peers_connected = True
-            dist.barrier()   # every home region is complete before anyone reads it
+            if self._eng.steal:
+                self._eng.queue_reset()
+            dist.barrier()   # home regions complete and queue words reset before anyone reads them
         self._eng.run(self._out, self._flags, host_items=host_items, device_items=device_items,
                       parsed_stride=stride)
-        if self._eng.peer_tier:
-            import torch.distributed as dist
-            dist.barrier()   # peers are done reading our home region
+        if shared:
+            dist.barrier()   # peers are done reading our home region and queue word
         if self.world > 1 and gather:
             gather_triangle(self._out, self._flags)
         values = self._out.cpu().numpy()

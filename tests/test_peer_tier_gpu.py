@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, ret):
+def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -28,7 +28,17 @@ def _rank(rank, world, port, ret):
         from paper_2009_04755_b200.apps import PCEApp
         from paper_2009_04755_b200.engine import AllPairsEngine
         app = PCEApp(26, side=256, cameras=3, seed=17, device=0)
-        eng = AllPairsEngine(app, leaf_block=4, device_slots=10, rank=rank, world=world, peer_tier=True)
+        eng = AllPairsEngine(app, leaf_block=4, device_slots=10, rank=rank, world=world, peer_tier=True,
+                             steal_chunk=steal_chunk)
+        if rank == 0 and delay0 > 0:
+            # rank 0 starts late (after the barrier): rank 1 runs dry and steals from it
+            import time
+            inner = eng._eng.run
+
+            def late_run(*a, **kw):
+                time.sleep(delay0)
+                return inner(*a, **kw)
+            eng._eng.run = late_run
         res = eng.run(gather=False)
         ret.put((rank, res.values.copy(), res.flags.copy(), res.stats))
         eng.close()
@@ -36,14 +46,17 @@ def _rank(rank, world, port, ret):
         dist.destroy_process_group()
 
 
-def test_two_ranks_peer_fetch_match_oracle():
+@pytest.mark.parametrize("steal_chunk,delay0", [(0, 0.0), (1, 3.0)])
+def test_two_ranks_peer_fetch_match_oracle(steal_chunk, delay0):
+    """Exactly-once coverage and oracle parity with the peer tier and the cross-GPU
+    work queue; the second case delays rank 0 so rank 1 must steal from it."""
     import torch.multiprocessing as mp
     from oracle import pce as opce
     from paper_2009_04755_b200.apps import PCEApp
     ctx = mp.get_context("spawn")
     ret = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, ret)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, ret, steal_chunk, delay0)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted([ret.get(timeout=300) for _ in range(2)], key=lambda o: o[0])
@@ -61,3 +74,6 @@ def test_two_ranks_peer_fetch_match_oracle():
         assert st["loads"] == 13                                 # only home items preprocessed: R = 1
         assert st["peer_fetches"] > 0 and st["peer_bytes"] == st["peer_fetches"] * 256 * 256 * 4
     assert outs[0][3]["pairs_done"] + outs[1][3]["pairs_done"] == 26 * 25 // 2
+    if delay0 > 0:
+        assert outs[1][3]["steals"] >= 1                         # the idle rank stole from the late one
+        assert outs[1][3]["pairs_done"] > outs[0][3]["pairs_done"]
