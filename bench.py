@@ -46,7 +46,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4096, help="items (default: configs[1], 4,096)")
+    ap.add_argument("--items", type=int, default=4096, help="items (default: configs[1], 4,096)")
     ap.add_argument("--side", type=int, default=1024, help="pattern side (default 1024)")
     ap.add_argument("--leaf", type=int, default=8)
     ap.add_argument("--cameras", type=int, default=64)
@@ -183,7 +183,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n, side = args.n, args.side
+    n, side = args.items, args.side
     pairs_total = n * (n - 1) // 2
     cfg_name = {(4096, 1024): " (BASELINE configs[1])", (16384, 2048): " (BASELINE configs[2])"}.get((n, side), "")
     workload = f"PRNU PCE all-pairs, N={n} patterns of {side}x{side} fp32{cfg_name}"

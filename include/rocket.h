@@ -199,6 +199,10 @@ rk_status rk_engine_set_peer_homes(rk_engine* eng, int32_t world, void* const* d
  * rk_engine_queue_reset on every rank (own word <- its contiguous share), a
  * barrier, then rk_engine_run.  rk_engine_set_peer_queues takes every rank's
  * mapped word (own entry = local) once after the IPC exchange. */
+/* Peer-tier copy bandwidth: `bytes` from rank src_rank's home region into this
+ * rank's cache slots with the run's own D2D copies (NVLink), GB/s.  Clobbers
+ * the cache slots: call between runs only. */
+rk_status rk_engine_peer_bandwidth(rk_engine* eng, int32_t src_rank, size_t bytes, double* gb_per_s);
 rk_status rk_engine_queue_word(const rk_engine* eng, void** d_word);
 rk_status rk_engine_queue_reset(rk_engine* eng);
 rk_status rk_engine_set_peer_queues(rk_engine* eng, int32_t world, void* const* d_words);

@@ -432,7 +432,7 @@ rk_status rk_engine_set_profiling(rk_engine* e, int every, int max_samples) {
 rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride, double* d_out,
                         uint8_t* d_flags) {
   if (!e) return set_error(RK_ERR_VALUE, "null engine");
-  if (!h_parsed && !d_parsed && e->app->p.kind != RK_APP_SYNTHETIC)
+  if (!h_parsed && !d_parsed && e->app->p.kind != RK_APP_SYNTHETIC && e->home_slots == 0)
     return set_error(RK_ERR_VALUE, "need host or device parsed items");
   RK_CUDA(cudaSetDevice(e->device));
   const int32_t n = e->app->p.n;
@@ -702,6 +702,30 @@ rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_
     e->stats.loads += m;
   }
   RK_CUDA(cudaStreamSynchronize(e->stream));
+  return RK_OK;
+}
+
+rk_status rk_engine_peer_bandwidth(rk_engine* e, int32_t src_rank, size_t bytes, double* gb_per_s) {
+  if (!e || !gb_per_s) return set_error(RK_ERR_VALUE, "null argument");
+  if (!e->peers_ready || src_rank < 0 || src_rank >= e->p.world) return set_error(RK_ERR_VALUE, "peer tier not connected");
+  RK_CUDA(cudaSetDevice(e->device));
+  const size_t cap = std::min((size_t)e->home_slots, (size_t)e->p.device_slots) * e->slot_stride;
+  bytes = std::min(bytes, cap);
+  cudaEvent_t a, b;
+  RK_CUDA(cudaEventCreate(&a));
+  RK_CUDA(cudaEventCreate(&b));
+  RK_CUDA(cudaEventRecord(a, e->lstream));
+  // the same copy the run issues for a peer fetch, in slot-sized pieces
+  for (size_t off = 0; off < bytes; off += e->slot_stride)
+    RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + off, e->peer_home[src_rank] + off,
+                            std::min(e->slot_stride, bytes - off), cudaMemcpyDeviceToDevice, e->lstream));
+  RK_CUDA(cudaEventRecord(b, e->lstream));
+  RK_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  RK_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *gb_per_s = ms > 0.f ? (double)bytes / (ms * 1e-3) / 1e9 : 0.0;
   return RK_OK;
 }
 

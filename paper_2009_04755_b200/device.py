@@ -191,6 +191,12 @@ class DeviceEngine:
         if self.steal:
             check(lib.rk_engine_set_peer_queues(self.handle, self.world, queues))
 
+    def peer_bandwidth(self, src_rank: int, nbytes: int) -> float:
+        """GB/s of the peer-tier D2D copy from src_rank's home region (between runs only)."""
+        gbs = C.c_double()
+        check(lib.rk_engine_peer_bandwidth(self.handle, src_rank, nbytes, C.byref(gbs)))
+        return float(gbs.value)
+
     def queue_reset(self) -> None:
         """Own work-queue word <- this rank's share; every rank, then a barrier, before run()."""
         check(lib.rk_engine_queue_reset(self.handle))
