@@ -189,6 +189,10 @@ rk_status rk_engine_home_region(const rk_engine* eng, void** d_base, size_t* byt
 rk_status rk_engine_arena(const rk_engine* eng, void** d_base, size_t* slot_stride);
 /* Home item m (key = rank + m*world) is read at parsed + m*parsed_stride. */
 rk_status rk_engine_load_home(rk_engine* eng, const void* h_parsed, const void* d_parsed, size_t parsed_stride);
+/* The same for home items m0 .. m0+count-1 only (item m0 + q at parsed + q * parsed_stride),
+ * so a home region larger than the free HBM can be filled chunk by chunk. */
+rk_status rk_engine_load_home_range(rk_engine* eng, const void* h_parsed, const void* d_parsed, size_t parsed_stride,
+                                    int32_t m0, int32_t count);
 rk_status rk_engine_set_peer_homes(rk_engine* eng, int32_t world, void* const* d_home_bases);
 /* CUDA IPC of a device allocation (64-byte handle) for the peer tier. */
 /* Cross-GPU work queue (hierarchical stealing, engine.py:274-309 and

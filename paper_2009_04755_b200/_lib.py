@@ -118,6 +118,7 @@ SIGNATURES = [
     ("rk_engine_home_region", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     ("rk_engine_arena", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     ("rk_engine_load_home", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    ("rk_engine_load_home_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32]),
     ("rk_engine_set_peer_homes", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("rk_engine_peer_bandwidth", C.c_int, [C.c_void_p, C.c_int32, C.c_size_t, C.POINTER(C.c_double)]),
     ("rk_engine_queue_word", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -673,20 +673,26 @@ rk_status rk_engine_arena(const rk_engine* e, void** d_base, size_t* slot_stride
   return RK_OK;
 }
 
-rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride) {
+rk_status rk_engine_load_home_range(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride,
+                                    int32_t m0, int32_t count) {
   if (!e) return set_error(RK_ERR_VALUE, "null engine");
   if (e->home_slots == 0) return set_error(RK_ERR_VALUE, "engine was created without the peer tier");
+  if (!h_parsed && !d_parsed) return set_error(RK_ERR_VALUE, "need host or device parsed items");
   RK_CUDA(cudaSetDevice(e->device));
   const int32_t n = e->app->p.n;
   std::vector<LoadReq> home;
-  for (int32_t k = e->p.rank; k < n; k += e->p.world) home.push_back(LoadReq{k, e->p.device_slots + k / e->p.world});
+  for (int32_t m = m0; m < m0 + count; ++m) {
+    const int32_t k = e->p.rank + m * e->p.world;
+    if (m < 0 || k >= n) return set_error(RK_ERR_VALUE, "home item %d out of range", m);
+    home.push_back(LoadReq{k, e->p.device_slots + m});
+  }
   // flush_loads publishes into the tier; home slots live outside it, so load directly
   const size_t pbytes = e->app->parsed_bytes;
   for (size_t base = 0; base < home.size(); base += e->staging_items) {
     const int m = (int)std::min<size_t>(e->staging_items, home.size() - base);
     std::vector<int32_t> slots(m);
     for (int k = 0; k < m; ++k) slots[k] = home[base + k].slot;
-    // home item m (key rank + m*world) is at parsed + m * parsed_stride
+    // home item m0 + q (key rank + (m0 + q)*world) is at parsed + q * parsed_stride
     if (h_parsed) {
       for (int k = 0; k < m; ++k) {
         const char* src = static_cast<const char*>(h_parsed) + (base + k) * parsed_stride;
@@ -703,6 +709,13 @@ rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_
   }
   RK_CUDA(cudaStreamSynchronize(e->stream));
   return RK_OK;
+}
+
+rk_status rk_engine_load_home(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  const int32_t n = e->app->p.n;
+  const int32_t count = n > e->p.rank ? (n - e->p.rank + e->p.world - 1) / e->p.world : 0;
+  return rk_engine_load_home_range(e, h_parsed, d_parsed, parsed_stride, 0, count);
 }
 
 rk_status rk_engine_peer_bandwidth(rk_engine* e, int32_t src_rank, size_t bytes, double* gb_per_s) {

@@ -14,21 +14,23 @@
 // The oracle restating these definitions is oracle/pce.py (parity unpinned by
 // the reference, which has no PCE: SURVEY.md section 8(c)).
 //
-// Compare kernel (pce_cluster): one thread-block cluster per pair in flight,
-// persistent over the job's pairs.  The 2-D inverse FFT needs one global
-// transpose; its intermediate T (4 MiB per pair at 1024^2) lives in an L2-sized
-// per-cluster slot, so only (#clusters x 4 MiB) of T is ever live.  Per pair:
-//   column phase  CTA q: product S_a*conj(S_b) + inverse column FFTs of its
-//                 N/2/CL columns -> T (row-major, staged through shared memory)
-//   cluster barrier (release/acquire: T visible, L1 invalidated)
-//   row phase     CTA q: inverse row C2R FFTs (two rows per complex FFT) of its
-//                 N/CL rows with fused max/argmax/energy; CTA partial -> CTA 0 (DSMEM)
-//   cluster barrier; every CTA combines the CL partials (same result everywhere)
-//   window        6 warps recompute the 11 rows around the peak and add their
-//                 11x11 energy into CTA 0 (DSMEM red.add)
-//   cluster barrier; CTA 0 writes the PCE score (and match flag).
-// Each warp prefetches its next unit's lines into L1 while it computes, so
-// global latency is overlapped with the FFT arithmetic.
+// Compare kernel (pce_cluster<R, CL>, CL = 1 in production): persistent, one
+// CTA = one SM per pair in flight (148 pairs); its 8 warps form two
+// independent warp groups (named barriers), each feeding itself through its own
+// bulk-copy (TMA 1-D) + mbarrier pipeline.  The 2-D inverse FFT needs one global
+// transpose; its intermediate T (4 MiB per pair at 1024^2) goes to a per-CTA
+// slot in HBM.  Per pair:
+//   column phase  per 4-column slice of X and Y (refilled as soon as the products
+//                 X*conj(Y) are in registers): inverse column FFTs -> T in 8-row blocks
+//   CTA barrier   (+ fence.proxy.async: T's generic stores before the bulk reads)
+//   row phase     per 8-row block (double-buffered bulk copies): inverse row C2R
+//                 FFTs (two rows per complex FFT) with fused max/argmax/energy
+//   reduction     fixed-order combine of the warp partials (deterministic)
+//   window        6 warps recompute the 11 rows around the peak from staged
+//                 blocks and sum the 11x11 energy; one thread writes PCE + flag.
+// CL > 1 (a cluster per pair, DSMEM reductions, T kept in L2) is still
+// compilable for the measurements recorded below and in DESIGN.md.
+
 #include <math.h>
 #include <stdio.h>
 

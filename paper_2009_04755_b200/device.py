@@ -152,6 +152,13 @@ class DeviceEngine:
         torch.cuda.current_stream(self.device).synchronize()
         check(lib.rk_engine_load_home(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride))
 
+    def load_home_range(self, m0: int, count: int, *, host_items=None, device_items=None,
+                        parsed_stride: int = 0) -> None:
+        """Home items m0 .. m0+count-1 (item m0+q at items + q*parsed_stride)."""
+        torch.cuda.current_stream(self.device).synchronize()
+        check(lib.rk_engine_load_home_range(self.handle, _ptr(host_items), _ptr(device_items), parsed_stride,
+                                            m0, count))
+
     @property
     def steal(self) -> bool:
         return bool(self.engine_params.steal)

@@ -4,9 +4,9 @@
   python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \\
       --master-port 29600 tools/c3_run.py [--items 16384] [--side 2048] [--slots 4500]
 
-Each rank generates only its home patterns (k % world == rank: 32 GiB at 8
-GPUs), preprocesses them into its home region (rk_engine_load_home), frees the
-patterns, then runs its share of the quadtree leaves through the cross-GPU work
+Each rank generates only its home patterns (k % world == rank: 64 GiB at 4
+GPUs, 32 GiB at 8), 256 at a time, preprocesses them into its home region
+(rk_engine_load_home_range), then runs its share of the quadtree leaves through the cross-GPU work
 queue (stealing on), fetching every other item from its home GPU over NVLink
 into its device slot tier.  Reported (one JSON line, rank 0):
 
@@ -66,17 +66,21 @@ def main():
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
 
-    # home patterns only (the load stage: generation is not timed)
+    # home patterns only, generated chunk by chunk (the load stage: generation untimed),
+    # each chunk preprocessed into the home region (synchronous, timed)
     home = list(range(rank, n, world))
-    raw = torch.empty(len(home) * ss, dtype=torch.float32, device="cuda")
-    for m, k in enumerate(home):
-        device.synth_prnu(side, side, k, 1, args.cameras, args.seed, raw.narrow(0, m * ss, ss))
-    torch.cuda.synchronize()
+    chunk = 256
+    raw = torch.empty(chunk * ss, dtype=torch.float32, device="cuda")
     dist.barrier()
-
-    t0 = time.perf_counter()
-    eng.load_home(device_items=raw, parsed_stride=ss * 4)      # synchronous
-    t_home = time.perf_counter() - t0
+    t_home = 0.0
+    for m0 in range(0, len(home), chunk):
+        cnt = min(chunk, len(home) - m0)
+        for q in range(cnt):
+            device.synth_prnu(side, side, home[m0 + q], 1, args.cameras, args.seed, raw.narrow(0, q * ss, ss))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.load_home_range(m0, cnt, device_items=raw, parsed_stride=ss * 4)
+        t_home += time.perf_counter() - t0
     del raw
     torch.cuda.empty_cache()
     eng.connect_peers()
