@@ -466,12 +466,13 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->loads_unsynced = false;
     RK_TRY(rk_ncc_gram(e->app, e->arena, e->slot_stride, e->tier->capacity, e->p.rank, e->p.world, d_out, d_flags,
                        e->stream));
-    const int side = (n + 127) / 128;
+    const int tile = ncc_gram_tile(n);
+    const int side = (n + tile - 1) / tile;
     int64_t mine = 0;
     for (int ti = 0, t = 0; ti < side; ++ti)
       for (int tj = ti; tj < side; ++tj, ++t)
         if (t % e->p.world == e->p.rank)
-          mine += region_pairs(ti * 128, std::min(n, ti * 128 + 128), tj * 128, std::min(n, tj * 128 + 128));
+          mine += region_pairs(ti * tile, std::min(n, ti * tile + tile), tj * tile, std::min(n, tj * tile + tile));
     e->stats.pairs_done += mine;
     e->stats.tiles += 1;
     RK_CUDA(cudaStreamSynchronize(e->stream));

@@ -105,6 +105,9 @@ rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, cons
                         double* d_out, uint8_t* d_flags, cudaStream_t s);
 void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, float* mean_part, cudaStream_t s);
 
+// NCC Gram tile side for n items (256: CTA-pair kernel, 128: single-CTA kernel)
+int ncc_gram_tile(int n);
+
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s);
 

@@ -28,7 +28,10 @@ namespace {
 
 constexpr int kTile = 128;          // items per Gram tile side (UMMA M = N = 128)
 constexpr int kBK = 32;             // fp32 elements per 128-B swizzled smem row (one TMA box row)
-constexpr int kStages = 4;
+#ifndef NCC_STAGES
+#define NCC_STAGES 6
+#endif
+constexpr int kStages = NCC_STAGES;  // 6 x 32 KiB in flight per SM (K = 1M streams: latency-bound at 4)
 constexpr int kStageBytes = 2 * kTile * kBK * 4;   // A + B tiles: 32 KiB
 constexpr int kGramThreads = 128;   // 4 warps: TMA producer, MMA issuer, all four in the epilogue
 
@@ -174,6 +177,36 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
   for (int k = 0; k < 32; ++k) r[k] = __uint_as_float(u[k]);
 }
 
+
+// ---- CTA-pair (cta_group::2) variants: UMMA M = N = 256 over two SMs ----------
+// Each CTA of the pair stages 128 rows of A and 128 rows of B (the same smem
+// offsets in both); the leader's single thread issues the MMA, which reads both
+// CTAs' tiles, and each CTA's TMEM receives its 128 accumulator rows x 256
+// columns.  Operand bytes per SM per MMA flop are half of the 128x128 kernel's.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+
+// arrive on `bar` (same smem offset) in both CTAs of the pair once the issued MMAs retire
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+
 // One CTA per upper-triangle 128x128 tile of items (tiles dealt to ranks).
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_constant__ CUtensorMap tmap, int n,
                                                                    int64_t d, int tiles_per_side, int rank, int world,
@@ -273,9 +306,121 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTile));
 }
 
+
+constexpr int kTile2 = 256;   // items per CTA-pair tile side
+
+// One CTA pair (cluster of 2) per upper-triangle 256x256 tile of items.
+__global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid_constant__ CUtensorMap tmap, int n,
+                                                                    int64_t d, int tiles_per_side, int rank,
+                                                                    int world, double* __restrict__ out,
+                                                                    uint8_t* __restrict__ flags, double threshold) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+
+  int t = (blockIdx.x >> 1) * world + rank;
+  int ti = 0;
+  while (t >= tiles_per_side - ti) {
+    t -= tiles_per_side - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int row0 = ti * kTile2 + (int)cta * kTile, col0 = tj * kTile2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kTile2));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const int kblocks = (int)(d / kBK);
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer (both CTAs): own A and B halves, completion on the leader's barrier ----
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      mbar_wait(&empty_bar[s], ph ^ 1u);
+      uint8_t* a = smem + (size_t)s * kStageBytes;
+      uint8_t* b = a + kTile * kBK * 4;
+      if (leader) mbar_expect_tx(&full_bar[s], 2 * kStageBytes);   // both CTAs' bytes
+      const uint32_t fb = dsmem_addr(&full_bar[s], 0);
+      tma_load_2d_pair(a, &tmap, kb * kBK, row0, fb);
+      tma_load_2d_pair(b, &tmap, kb * kBK, col0 + (int)cta * kTile, fb);
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---- MMA issuer (leader CTA, single thread) ----
+    constexpr uint32_t idesc = idesc_tf32(kTile2, kTile2);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      mbar_wait(&full_bar[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a = smem_u32(smem + (size_t)s * kStageBytes);
+      const uint32_t b = a + kTile * kBK * 4;
+#pragma unroll
+      for (int k = 0; k < kBK / 8; ++k)
+        umma_tf32_pair(tmem, umma_smem_desc_sw128(a + k * 32), umma_smem_desc_sw128(b + k * 32), idesc,
+                       (kb | k) != 0);
+      umma_commit_pair(&empty_bar[s]);   // stage free in both CTAs once these MMAs retire
+    }
+    umma_commit_pair(&done_bar);
+  }
+
+  // ---- epilogue: each CTA drains its 128 rows x 256 columns ----
+  __syncwarp();
+  mbar_wait(&done_bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int i = row0 + warp * 32 + lane;
+  const int64_t nn = n;
+#pragma unroll 1
+  for (int c = 0; c < kTile2; c += 32) {
+    float r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
+    if (i < n) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int j = col0 + c + k;
+        if (j > i && j < n) {
+          const int64_t pid = (int64_t)i * (2 * nn - i - 1) / 2 + (j - i - 1);
+          out[pid] = (double)r[k];
+          if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | ((double)r[k] >= threshold ? 2 : 0));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTile2));
+}
+
 size_t gram_smem() { return (size_t)kStages * kStageBytes + 1024; }
 
 }  // namespace
+
+int ncc_gram_tile(int n) {
+#ifndef NCC_GRAM_1CTA
+  if (n > kTile) return kTile2;
+#endif
+  (void)n;
+  return kTile;
+}
 
 rk_status tensor_map_encoder(EncodeTiledFn* fn) {
   static EncodeTiledFn cached = nullptr;
@@ -299,6 +444,7 @@ rk_status ncc_init(rk_app* app) {
   app->parsed_bytes = (size_t)d * sizeof(float);
   RK_CUDA(cudaMalloc(&app->ncc.part, sizeof(double) * 2 * 64 * kMaxBatch));
   RK_CUDA(cudaFuncSetAttribute(ncc_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem()));
+  RK_CUDA(cudaFuncSetAttribute(ncc_gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem()));
   return RK_OK;
 }
 
@@ -365,6 +511,32 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+#ifndef NCC_GRAM_1CTA
+  if (ncc_gram_tile(n) == kTile2) {
+    // CTA-pair kernel: 256x256 tiles, one cluster of 2 per tile
+    const int side = (n + kTile2 - 1) / kTile2;
+    const int tiles = side * (side + 1) / 2;
+    const int mine = (tiles - rank + world - 1) / world;
+    if (mine <= 0) return RK_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * mine);
+    cfg.blockDim = dim3(kGramThreads);
+    cfg.dynamicSmemBytes = gram_smem();
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, n, d, side, rank, world, d_out, d_flags,
+                               threshold_or_nan(app)));
+    app->launches += 1;
+    RK_CUDA(cudaGetLastError());
+    return RK_OK;
+  }
+#endif
   const int side = (n + kTile - 1) / kTile;
   const int tiles = side * (side + 1) / 2;
   const int mine = (tiles - rank + world - 1) / world;

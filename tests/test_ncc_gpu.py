@@ -24,8 +24,10 @@ def make_items(n, side, seed=3, cameras=4):
     return buf
 
 
-@pytest.mark.parametrize("n", [37, 200])
+@pytest.mark.parametrize("n", [37, 200, 600])
 def test_gram_matches_oracle(n):
+    """37: single-CTA 128x128 kernel; 200, 600: CTA-pair 256x256 kernel (one tile
+    with zero-filled rows beyond n; six tiles)."""
     _l, device = _mods()
     side = 256
     items = make_items(n, side)
