@@ -96,6 +96,11 @@ void rk_app_destroy(rk_app* app);
 size_t rk_app_slot_bytes(const rk_app* app);
 /* Bytes of one parsed item as handed to rk_preprocess. */
 size_t rk_app_parsed_bytes(const rk_app* app);
+/* Slots are interleaved in groups of this many (1 = every slot contiguous).  NCC
+ * uses 128: group g's 128 slots share the region [g*128*stride, (g+1)*128*stride)
+ * as [D/1024][128][1024] floats, so one TMA box (128 items x 32 floats) spans
+ * 512 KiB instead of 128 pages.  Arenas must hold a multiple of this many slots. */
+int32_t rk_app_slot_group(const rk_app* app);
 
 /* Application.preprocess for a batch of items already resident on the device
  * (replaces apps.py:304-318 and the gpu-lane preprocess at engine.py:464-472).

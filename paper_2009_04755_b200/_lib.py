@@ -95,6 +95,7 @@ SIGNATURES = [
     ("rk_app_destroy", None, [C.c_void_p]),
     ("rk_app_slot_bytes", C.c_size_t, [C.c_void_p]),
     ("rk_app_parsed_bytes", C.c_size_t, [C.c_void_p]),
+    ("rk_app_slot_group", C.c_int32, [C.c_void_p]),
     ("rk_preprocess", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_size_t,
                                 C.POINTER(C.c_int32), C.c_void_p]),
     ("rk_compare_pairs", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(Pair), C.c_int,

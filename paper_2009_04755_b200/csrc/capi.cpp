@@ -1,4 +1,5 @@
 // extern "C" entry points of librocket (see include/rocket.h).
+#include <stdlib.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -24,6 +25,12 @@ rk_status set_error(rk_status st, const char* fmt, ...) {
 
 rk_status check_cuda(cudaError_t err, const char* what) {
   return set_error(RK_ERR_DEVICE, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
+}
+
+size_t stride_pad(const char* env, size_t dflt) {
+  const char* v = getenv(env);
+  if (!v || !*v) return dflt;
+  return (size_t)strtoull(v, nullptr, 10) / 256 * 256;
 }
 
 double threshold_or_nan(const rk_app* app) { return app->p.threshold; }
@@ -165,6 +172,7 @@ void rk_app_destroy(rk_app* app) {
 
 size_t rk_app_slot_bytes(const rk_app* app) { return app ? app->slot_bytes : 0; }
 size_t rk_app_parsed_bytes(const rk_app* app) { return app ? app->parsed_bytes : 0; }
+int32_t rk_app_slot_group(const rk_app* app) { return app ? app->slot_group : 1; }
 
 rk_status rk_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                         size_t slot_stride, const int32_t* h_slot_idx, void* stream) {

@@ -243,13 +243,14 @@ struct rk_engine {
   int64_t steals = 0;
   void* arena = nullptr;
   size_t slot_stride = 0;
+  size_t arena_slots = 0;           // device_slots rounded up to the app's slot group
   void* staging = nullptr;
   int staging_items = 0;
   rk::SlotTier* tier = nullptr;
   rk_engine_stats stats{};
   // peer-GPU tier (distcache.py owner_of: home(k) = k mod world): this rank's home
-  // items live at arena slots [device_slots, device_slots + home_slots), item k at
-  // device_slots + k / world; other ranks' home regions are IPC-mapped
+  // items live at arena slots [arena_slots, arena_slots + home_slots), item k at
+  // arena_slots + k / world; other ranks' home regions are IPC-mapped
   int home_slots = 0;
   std::vector<const char*> peer_home;   // per rank: base of its home region (own entry = local)
   bool peers_ready = false;
@@ -365,7 +366,7 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
     rk_engine_destroy(e);
     return s;
   };
-  e->slot_stride = (e->app->slot_bytes + 255) / 256 * 256;
+  e->slot_stride = (e->app->slot_bytes + 255) / 256 * 256 + stride_pad("RK_SLOT_PAD", 0);
   cudaError_t ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaStreamCreate"));
   ce = cudaStreamCreateWithFlags(&e->lstream, cudaStreamNonBlocking);
@@ -375,7 +376,10 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaEventCreate"));
   if (params->peer_tier && params->world > 1)
     e->home_slots = (app_params->n + params->world - 1) / params->world;
-  const size_t arena_bytes = e->slot_stride * ((size_t)params->device_slots + e->home_slots);
+  // interleaved slot groups (rk_app_slot_group): whole groups only
+  const size_t g = (size_t)std::max(1, e->app->slot_group);
+  e->arena_slots = ((size_t)params->device_slots + g - 1) / g * g;
+  const size_t arena_bytes = e->slot_stride * (e->arena_slots + e->home_slots);
   ce = cudaMalloc(&e->arena, arena_bytes + 256);   // + the work-queue word (shared with the home region over IPC)
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(slot arena)"));
   e->qword = reinterpret_cast<unsigned long long*>(static_cast<char*>(e->arena) + arena_bytes);
@@ -464,8 +468,8 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     for (int32_t k = 0; k < n; ++k) e->tier->release(e->tier->find(k));
     if (e->loads_unsynced) RK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_loaded, 0));
     e->loads_unsynced = false;
-    RK_TRY(rk_ncc_gram(e->app, e->arena, e->slot_stride, e->tier->capacity, e->p.rank, e->p.world, d_out, d_flags,
-                       e->stream));
+    RK_TRY(rk_ncc_gram(e->app, e->arena, e->slot_stride, (int32_t)e->arena_slots, e->p.rank, e->p.world, d_out,
+                       d_flags, e->stream));
     const int tile = ncc_gram_tile(n);
     const int side = (n + tile - 1) / tile;
     int64_t mine = 0;
@@ -514,7 +518,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     pinned.clear();
     for (int32_t k : keys) {
       if (peer && k % world == e->p.rank) {
-        slot_of[k] = e->p.device_slots + k / world;   // home item: resident for the whole run
+        slot_of[k] = (int32_t)e->arena_slots + k / world;   // home item: resident for the whole run
         continue;
       }
       const int64_t evictions_before = e->tier->evictions;
@@ -662,7 +666,7 @@ extern "C" {
 
 rk_status rk_engine_home_region(const rk_engine* e, void** d_base, size_t* bytes) {
   if (!e || !d_base || !bytes) return set_error(RK_ERR_VALUE, "null argument");
-  *d_base = static_cast<char*>(e->arena) + (size_t)e->p.device_slots * e->slot_stride;
+  *d_base = static_cast<char*>(e->arena) + e->arena_slots * e->slot_stride;
   *bytes = (size_t)e->home_slots * e->slot_stride;
   return RK_OK;
 }
@@ -685,7 +689,7 @@ rk_status rk_engine_load_home_range(rk_engine* e, const void* h_parsed, const vo
   for (int32_t m = m0; m < m0 + count; ++m) {
     const int32_t k = e->p.rank + m * e->p.world;
     if (m < 0 || k >= n) return set_error(RK_ERR_VALUE, "home item %d out of range", m);
-    home.push_back(LoadReq{k, e->p.device_slots + m});
+    home.push_back(LoadReq{k, (int32_t)e->arena_slots + m});
   }
   // flush_loads publishes into the tier; home slots live outside it, so load directly
   const size_t pbytes = e->app->parsed_bytes;

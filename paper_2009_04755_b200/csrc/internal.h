@@ -67,13 +67,15 @@ struct PceState {
   float2* U = nullptr;     // batch * (N/2) * N: preprocess row-pass output
   float* mean_part = nullptr;    // batch * 64 partial sums
   int clusters = 0;        // co-resident compare clusters (= pairs in flight)
-  float2* T = nullptr;     // clusters * (N/2) * N: column-pass output, one slot per cluster
+  float2* T = nullptr;     // clusters * t_stride: column-pass output, one slot per cluster
+  size_t t_stride = 0;     // float2 between T slots: (N/2)*N + padding (breaks the power-of-two stride)
   PceJob* job = nullptr;   // host staging of the launch parameters
 };
 
 struct CvState {};
 struct NccState {
   double* part = nullptr;   // per-CTA (sum, sum of squares) partials of the preprocess
+  int64_t kc = 0;           // interleave run (floats): 1024 when D % 1024 == 0, else D (contiguous slots)
 };
 struct GmmState {};
 
@@ -85,6 +87,7 @@ struct rk_app {
   size_t slot_bytes = 0;
   size_t parsed_bytes = 0;
   int64_t launches = 0;    // kernels launched through this app (for bench accounting)
+  int32_t slot_group = 1;  // slots interleaved in groups of this many (rk_app_slot_group)
   rk::PceState pce;
   rk::NccState ncc;
 };
@@ -129,6 +132,8 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
                    double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 double threshold_or_nan(const rk_app* app);
+// Padding (bytes) added to power-of-two per-item / per-CTA strides (env RK_SLOT_PAD / RK_T_PAD)
+size_t stride_pad(const char* env, size_t dflt);
 
 // cuTensorMapEncodeTiled, fetched from the driver through the runtime (no -lcuda).
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

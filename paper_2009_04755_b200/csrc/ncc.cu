@@ -34,6 +34,18 @@ constexpr int kBK = 32;             // fp32 elements per 128-B swizzled smem row
 constexpr int kStages = NCC_STAGES;  // 6 x 32 KiB in flight per SM (K = 1M streams: latency-bound at 4)
 constexpr int kStageBytes = 2 * kTile * kBK * 4;   // A + B tiles: 32 KiB
 constexpr int kGramThreads = 128;   // 4 warps: TMA producer, MMA issuer, all four in the epilogue
+constexpr int kGroup = 128;         // slots per interleaved group (rk_app_slot_group)
+constexpr int kKC = 1024;           // interleave run (floats) when D % 1024 == 0
+
+// Byte offset of element e of slot s.  Group g = s / 128 owns the region
+// [g*128*stride, (g+1)*128*stride) laid out as [D/kc][128][kc] floats, so the
+// 128 items of a Gram tile row block at one k sit within 128*kc*4 bytes (one
+// 512 KiB span) instead of 128 different pages: the TMA loads stop missing the
+// TLB once the arena outgrows its reach (measured: 16 GiB arena -> 250 TF/s).
+__host__ __device__ __forceinline__ size_t ncc_off(int64_t s, int64_t e, int64_t kc, size_t stride) {
+  return (size_t)(s / kGroup) * kGroup * stride +
+         (size_t)(((e / kc) * kGroup + (s % kGroup)) * kc + e % kc) * sizeof(float);
+}
 
 // ---------------------------------------------------------------------------
 // preprocess: per item two passes -- (sum, sum of squares) then normalise
@@ -71,8 +83,9 @@ __global__ void __launch_bounds__(256) ncc_moments(const float* __restrict__ pix
 }
 
 __global__ void __launch_bounds__(256) ncc_normalise(const float* __restrict__ pix, size_t stride_f, int64_t d,
-                                                     const double* __restrict__ part, int nparts, char* slots,
-                                                     size_t slot_stride, SlotList dst, int* __restrict__ status) {
+                                                     int64_t kc, const double* __restrict__ part, int nparts,
+                                                     char* slots, size_t slot_stride, SlotList dst,
+                                                     int* __restrict__ status) {
   const int item = blockIdx.y;
   __shared__ float s_mu, s_inv;
   if (threadIdx.x == 0) {
@@ -90,30 +103,37 @@ __global__ void __launch_bounds__(256) ncc_normalise(const float* __restrict__ p
   __syncthreads();
   const float mu = s_mu, inv = s_inv;
   const float4* x = reinterpret_cast<const float4*>(pix + (size_t)item * stride_f);
-  float4* y = reinterpret_cast<float4*>(slots + (size_t)dst.idx[item] * slot_stride);
+  const int64_t sl = dst.idx[item];
+  // runs of kc floats: the first run's address plus the run stride (128 * kc floats)
+  float4* y0 = reinterpret_cast<float4*>(slots + ncc_off(sl, 0, kc, slot_stride));
+  const int64_t run4 = kc / 4, jump4 = (int64_t)kGroup * kc / 4;
   const int64_t n4 = d / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = __ldg(x + i);
-    y[i] = make_float4((v.x - mu) * inv, (v.y - mu) * inv, (v.z - mu) * inv, (v.w - mu) * inv);
+    y0[(i / run4) * jump4 + i % run4] = make_float4((v.x - mu) * inv, (v.y - mu) * inv, (v.z - mu) * inv, (v.w - mu) * inv);
   }
 }
 
 // ---------------------------------------------------------------------------
 // per-pair path: one warp per pair, fp32 dot with float4 loads
 __global__ void __launch_bounds__(256) ncc_pairs_kernel(PairBatch b, const char* __restrict__ slots, size_t slot_stride,
-                                                        int64_t d, double* __restrict__ out,
+                                                        int64_t d, int64_t kc, double* __restrict__ out,
                                                         uint8_t* __restrict__ flags, double threshold) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * 8 + warp;
   if (p >= b.npairs) return;
-  const float4* x = reinterpret_cast<const float4*>(slots + (size_t)b.slot_a[p] * slot_stride);
-  const float4* y = reinterpret_cast<const float4*>(slots + (size_t)b.slot_b[p] * slot_stride);
+  const float4* x = reinterpret_cast<const float4*>(slots + ncc_off(b.slot_a[p], 0, kc, slot_stride));
+  const float4* y = reinterpret_cast<const float4*>(slots + ncc_off(b.slot_b[p], 0, kc, slot_stride));
   float acc0 = 0.f, acc1 = 0.f;
-  const int64_t n4 = d / 4;
-  for (int64_t i = lane; i < n4; i += 32) {
-    const float4 u = __ldg(x + i), v = __ldg(y + i);
-    acc0 = fmaf(u.x, v.x, fmaf(u.y, v.y, acc0));
-    acc1 = fmaf(u.z, v.z, fmaf(u.w, v.w, acc1));
+  const int64_t run4 = kc / 4, jump4 = (int64_t)kGroup * kc / 4;
+  for (int64_t r = 0; r < d / kc; ++r) {      // runs of kc floats, 128*kc apart
+    const float4* xr = x + r * jump4;
+    const float4* yr = y + r * jump4;
+    for (int64_t i = lane; i < run4; i += 32) {
+      const float4 u = __ldg(xr + i), v = __ldg(yr + i);
+      acc0 = fmaf(u.x, v.x, fmaf(u.y, v.y, acc0));
+      acc1 = fmaf(u.z, v.z, fmaf(u.w, v.w, acc1));
+    }
   }
   double acc = (double)acc0 + (double)acc1;
 #pragma unroll
@@ -142,10 +162,14 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// 128 rows (items row0 .. row0+127, row0 % 128 == 0) x 32 floats at element e of
+// the interleaved slot tensor (see ncc_off): coordinates (e % kc, 0, e / kc, row0 / 128)
+__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, int64_t e, int64_t kc, int row0,
+                                              uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"((int)(e % kc)), "r"(0), "r"((int)(e / kc)), "r"(row0 / kGroup),
+        "r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -183,12 +207,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
 // offsets in both); the leader's single thread issues the MMA, which reads both
 // CTAs' tiles, and each CTA's TMEM receives its 128 accumulator rows x 256
 // columns.  Operand bytes per SM per MMA flop are half of the 128x128 kernel's.
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
-                                                 uint32_t bar_cluster) {
+__device__ __forceinline__ void tma_load_rows_pair(void* dst, const CUtensorMap* map, int64_t e, int64_t kc, int row0,
+                                                   uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3}], [%4];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"((int)(e % kc)), "r"(0), "r"((int)(e / kc)), "r"(row0 / kGroup),
+        "r"(bar_cluster) : "memory");
 }
 
 __device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -209,7 +234,7 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 
 // One CTA per upper-triangle 128x128 tile of items (tiles dealt to ranks).
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_constant__ CUtensorMap tmap, int n,
-                                                                   int64_t d, int tiles_per_side, int rank, int world,
+                                                                   int64_t d, int64_t kc, int tiles_per_side, int rank, int world,
                                                                    double* __restrict__ out,
                                                                    uint8_t* __restrict__ flags, double threshold) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -256,8 +281,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
       uint8_t* a = smem + (size_t)s * kStageBytes;
       uint8_t* b = a + kTile * kBK * 4;
       mbar_expect_tx(&full_bar[s], kStageBytes);
-      tma_load_2d(a, &tmap, kb * kBK, row0, &full_bar[s]);
-      tma_load_2d(b, &tmap, kb * kBK, col0, &full_bar[s]);
+      tma_load_rows(a, &tmap, (int64_t)kb * kBK, kc, row0, &full_bar[s]);
+      tma_load_rows(b, &tmap, (int64_t)kb * kBK, kc, col0, &full_bar[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
@@ -308,10 +333,19 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
 
 
 constexpr int kTile2 = 256;   // items per CTA-pair tile side
+#ifndef NCC_KCHUNK
+#define NCC_KCHUNK 2048
+#endif
+constexpr int kChunkBlocks = NCC_KCHUNK;   // k-blocks (x 32 floats) per launch: 64K floats
 
 // One CTA pair (cluster of 2) per upper-triangle 256x256 tile of items.
+// K is processed in chunks [kb0, kb1) of k-blocks, one launch each: every CTA of
+// a launch streams the same K window, so the tiles sharing an operand row block
+// read it while it is still in L2 (with K = 1M in one launch the CTAs drift
+// apart and most operand reads miss L2).  Chunk 0 stores, later chunks add
+// (fp64, fixed launch order: deterministic); the last chunk writes the flags.
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid_constant__ CUtensorMap tmap, int n,
-                                                                    int64_t d, int tiles_per_side, int rank,
+                                                                    int64_t d, int64_t kc, int kb0, int kb1, int tiles_per_side, int rank,
                                                                     int world, double* __restrict__ out,
                                                                     uint8_t* __restrict__ flags, double threshold) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -349,7 +383,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
   cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const int kblocks = (int)(d / kBK);
+  const int kblocks = kb1 - kb0;
+  const bool first = kb0 == 0;
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer (both CTAs): own A and B halves, completion on the leader's barrier ----
@@ -359,10 +394,16 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
       mbar_wait(&empty_bar[s], ph ^ 1u);
       uint8_t* a = smem + (size_t)s * kStageBytes;
       uint8_t* b = a + kTile * kBK * 4;
+#ifdef NCC_PROBE_NOTMA   // diagnostic: MMA rate on stale tiles
+      if (leader) mbar_expect_tx(&full_bar[s], 0);
+      (void)a;
+      (void)b;
+#else
       if (leader) mbar_expect_tx(&full_bar[s], 2 * kStageBytes);   // both CTAs' bytes
       const uint32_t fb = dsmem_addr(&full_bar[s], 0);
-      tma_load_2d_pair(a, &tmap, kb * kBK, row0, fb);
-      tma_load_2d_pair(b, &tmap, kb * kBK, col0 + (int)cta * kTile, fb);
+      tma_load_rows_pair(a, &tmap, (int64_t)(kb0 + kb) * kBK, kc, row0, fb);
+      tma_load_rows_pair(b, &tmap, (int64_t)(kb0 + kb) * kBK, kc, col0 + (int)cta * kTile, fb);
+#endif
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---- MMA issuer (leader CTA, single thread) ----
@@ -374,10 +415,15 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a = smem_u32(smem + (size_t)s * kStageBytes);
       const uint32_t b = a + kTile * kBK * 4;
+#ifndef NCC_PROBE_NOMMA   // diagnostic: operand feed rate without the MMAs
 #pragma unroll
       for (int k = 0; k < kBK / 8; ++k)
         umma_tf32_pair(tmem, umma_smem_desc_sw128(a + k * 32), umma_smem_desc_sw128(b + k * 32), idesc,
                        (kb | k) != 0);
+#else
+      (void)a;
+      (void)b;
+#endif
       umma_commit_pair(&empty_bar[s]);   // stage free in both CTAs once these MMAs retire
     }
     umma_commit_pair(&done_bar);
@@ -399,8 +445,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
         const int j = col0 + c + k;
         if (j > i && j < n) {
           const int64_t pid = (int64_t)i * (2 * nn - i - 1) / 2 + (j - i - 1);
-          out[pid] = (double)r[k];
-          if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | ((double)r[k] >= threshold ? 2 : 0));
+          const double v = first ? (double)r[k] : out[pid] + (double)r[k];
+          out[pid] = v;
+          if (flags && (int64_t)kb1 * kBK >= d) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
         }
       }
     }
@@ -442,6 +489,8 @@ rk_status ncc_init(rk_app* app) {
     return set_error(RK_ERR_UNSUPPORTED, "NCC item size %lld must be a positive multiple of %d", (long long)d, kBK);
   app->slot_bytes = (size_t)d * sizeof(float);
   app->parsed_bytes = (size_t)d * sizeof(float);
+  app->ncc.kc = (d % kKC == 0) ? kKC : d;
+  app->slot_group = kGroup;
   RK_CUDA(cudaMalloc(&app->ncc.part, sizeof(double) * 2 * 64 * kMaxBatch));
   RK_CUDA(cudaFuncSetAttribute(ncc_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem()));
   RK_CUDA(cudaFuncSetAttribute(ncc_gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem()));
@@ -470,7 +519,7 @@ rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
     SlotList dst;
     dst.n = m;
     for (int k = 0; k < m; ++k) dst.idx[k] = h_slot_idx[base + k];
-    ncc_normalise<<<dim3(kParts, m), 256, 0, s>>>(px, stride_f, d, app->ncc.part, kParts,
+    ncc_normalise<<<dim3(kParts, m), 256, 0, s>>>(px, stride_f, d, app->ncc.kc, app->ncc.part, kParts,
                                                  static_cast<char*>(d_slots), slot_stride, dst, d_status);
     app->launches += 2;
     RK_CUDA(cudaGetLastError());
@@ -486,7 +535,8 @@ rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
 rk_status ncc_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
                       uint8_t* d_flags, cudaStream_t s) {
   const int64_t d = (int64_t)app->p.height * app->p.width;
-  ncc_pairs_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const char*>(d_slots), slot_stride, d, d_out,
+  ncc_pairs_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const char*>(d_slots), slot_stride, d,
+                                                       app->ncc.kc, d_out,
                                                        d_flags, threshold_or_nan(app));
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
@@ -502,12 +552,16 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
   if (world < 1 || rank < 0 || rank >= world) return set_error(RK_ERR_VALUE, "bad rank/world");
   EncodeTiledFn encode = nullptr;
   RK_TRY(tensor_map_encoder(&encode));
+  if (n_rows % kGroup != 0)
+    return set_error(RK_ERR_VALUE, "Gram arena must hold whole slot groups of %d (got %d slots)", kGroup, n_rows);
+  // the interleaved slot layout as a 4-D tensor: (e % kc, slot % 128, e / kc, slot / 128)
+  const int64_t kc = app->ncc.kc;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n_rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)slot_stride};
-  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kTile};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(d_slots), dims, strides, box,
+  const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)kGroup, (cuuint64_t)(d / kc), (cuuint64_t)(n_rows / kGroup)};
+  const cuuint64_t strides[3] = {(cuuint64_t)kc * 4, (cuuint64_t)kGroup * kc * 4, (cuuint64_t)kGroup * slot_stride};
+  const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)kTile, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(d_slots), dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
@@ -530,9 +584,13 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, n, d, side, rank, world, d_out, d_flags,
-                               threshold_or_nan(app)));
-    app->launches += 1;
+    const int kblocks = (int)(d / kBK);
+    for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkBlocks) {
+      const int kb1 = std::min(kblocks, kb0 + kChunkBlocks);
+      RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, n, d, kc, kb0, kb1, side, rank, world, d_out, d_flags,
+                                 threshold_or_nan(app)));
+      app->launches += 1;
+    }
     RK_CUDA(cudaGetLastError());
     return RK_OK;
   }
@@ -541,7 +599,7 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
   const int tiles = side * (side + 1) / 2;
   const int mine = (tiles - rank + world - 1) / world;
   if (mine <= 0) return RK_OK;
-  ncc_gram_kernel<<<mine, kGramThreads, gram_smem(), s>>>(map, n, d, side, rank, world, d_out, d_flags,
+  ncc_gram_kernel<<<mine, kGramThreads, gram_smem(), s>>>(map, n, d, kc, side, rank, world, d_out, d_flags,
                                                           threshold_or_nan(app));
   app->launches += 1;
   RK_CUDA(cudaGetLastError());

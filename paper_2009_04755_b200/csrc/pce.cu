@@ -199,7 +199,7 @@ __device__ unsigned long long g_pce_probe[148 * 2 * 8];
 
 template <int R, int CL>
 __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
-    const PceJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T,
+    const PceJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   float2* xbuf = xbufs + grp * R * R;
   float2* gb = gbufs + wg * 2 * kHalf;    // this warp group's 2 x 4N float2
-  float2* Tp = T + (size_t)cid * (N / 2) * N;
+  float2* Tp = T + (size_t)cid * t_stride;
   for (int i = tid; i < R * R; i += NT) tw[i] = tw_g[i];
   if (tid == 0) {
     for (int w = 0; w < 2; ++w)
@@ -554,7 +554,7 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
   const int clusters = std::min(st.clusters, n);
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
-  RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, (const float2*)st.tw, d_out,
+  RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, st.t_stride, (const float2*)st.tw, d_out,
                              d_flags, threshold_or_nan(app)));
   app->launches += 1;
   return RK_OK;
@@ -571,7 +571,8 @@ rk_status cluster_init(rk_app* app) {
   RK_CUDA(cudaOccupancyMaxActiveClusters(&clusters, pce_cluster<R, CL>, &cfg));
   if (clusters < 1) return set_error(RK_ERR_DEVICE, "pce_cluster: no cluster of %d CTAs fits", CL);
   st.clusters = clusters;
-  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * (size_t)(N / 2) * N * clusters));
+  st.t_stride = (size_t)(N / 2) * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
+  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * clusters));
   st.job = new PceJob();
   return RK_OK;
 }

@@ -257,7 +257,7 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, const char* __restrict__ slots,
-                                                            size_t slot_stride, float2* __restrict__ T,
+                                                            size_t slot_stride, float2* __restrict__ T, size_t t_stride,
                                                             const float2* __restrict__ tw_g, double* __restrict__ out,
                                                             uint8_t* __restrict__ flags, double threshold) {
   constexpr int kGW = kWarps / 2;                        // warps per warp group
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, c
   const bool leader = (tid % (kGW * 32)) == 0;
   float2* xbuf = xbufs + warp * kXbuf;
   float2* gb = gbufs + wg * 2 * kUnitF2;
-  float2* Tp = T + (size_t)blockIdx.x * NC * N;
+  float2* Tp = T + (size_t)blockIdx.x * t_stride;
   for (int i = tid; i < R * R; i += kWarps * 32) tw[i] = tw_g[i];
   if (tid == 0) {
     for (int w = 0; w < 2; ++w)
@@ -500,7 +500,8 @@ rk_status pce2k_init(rk_app* app) {
   RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pce2k_pair, kWarps * 32, kPairSmem));
   if (per_sm < 1) return set_error(RK_ERR_DEVICE, "pce2k_pair: does not fit on an SM");
   st.clusters = per_sm * sms;
-  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * (size_t)NC * N * st.clusters));
+  st.t_stride = (size_t)NC * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
+  RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * st.clusters));
   st.job = new PceJob();
   return RK_OK;
 }
@@ -535,7 +536,7 @@ rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, cons
     job.pairs[k].pid = pair_id(app->p.n, pairs[k].i, pairs[k].j);
   }
   const int grid = std::min(st.clusters, n);
-  pce2k_pair<<<grid, kWarps * 32, kPairSmem, s>>>(job, slots, slot_stride, st.T, st.tw, d_out, d_flags,
+  pce2k_pair<<<grid, kWarps * 32, kPairSmem, s>>>(job, slots, slot_stride, st.T, st.t_stride, st.tw, d_out, d_flags,
                                                    threshold_or_nan(app));
   app->launches += 1;
   RK_CUDA(cudaGetLastError());

@@ -38,6 +38,7 @@ class DeviceApp:
         self.slot_bytes = int(lib.rk_app_slot_bytes(handle))
         self.parsed_bytes = int(lib.rk_app_parsed_bytes(handle))
         self.slot_stride = (self.slot_bytes + 255) // 256 * 256
+        self.slot_group = int(lib.rk_app_slot_group(handle))
 
     def close(self) -> None:
         if self.handle:
@@ -51,6 +52,8 @@ class DeviceApp:
             pass
 
     def alloc_slots(self, count: int) -> torch.Tensor:
+        g = self.slot_group   # interleaved slot groups: whole groups only
+        count = (count + g - 1) // g * g
         return torch.empty(count * self.slot_stride, dtype=torch.uint8, device=f"cuda:{self.device}")
 
     def preprocess(self, parsed: torch.Tensor, parsed_stride: int, n_items: int, slots: torch.Tensor,
