@@ -42,8 +42,8 @@ rk_status synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, i
 rk_status cv_init(rk_app* app);
 rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                         size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s);
-rk_status cv_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
-                     uint8_t* d_flags, cudaStream_t s);
+rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                          double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 static rk_status check_pairs(const rk_app* app, const rk_pair* h_pairs, int n_pairs) {
   for (int k = 0; k < n_pairs; ++k) {
@@ -56,7 +56,8 @@ static rk_status check_pairs(const rk_app* app, const rk_pair* h_pairs, int n_pa
 }
 
 int batch_limit(const rk_app* app) {
-  if (app->p.kind == RK_APP_PCE) return kPipeMaxPairs;
+  // by-value pair lists of up to 1,024 pairs (PceJob) for the heavy apps
+  if (app->p.kind == RK_APP_PCE || app->p.kind == RK_APP_GMM || app->p.kind == RK_APP_CV) return kPipeMaxPairs;
   return kMaxBatch;
 }
 
@@ -64,9 +65,7 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
                         uint8_t* d_flags, cudaStream_t s) {
   switch (app->p.kind) {
     case RK_APP_SYNTHETIC: return synth_compare(app, b, d_out, d_flags, s);
-    case RK_APP_CV: return cv_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     case RK_APP_NCC: return ncc_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
-    case RK_APP_GMM: return gmm_compare(app, d_slots, slot_stride, b, d_out, d_flags, s);
     default: return set_error(RK_ERR_UNSUPPORTED, "compare not built for app kind %d", app->p.kind);
   }
 }
@@ -74,6 +73,8 @@ rk_status compare_batch(rk_app* app, const void* d_slots, size_t slot_stride, co
 rk_status compare_pairs(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* h_pairs, int n_pairs,
                         double* d_out, uint8_t* d_flags, cudaStream_t s) {
   if (app->p.kind == RK_APP_PCE) return pce_compare_list(app, d_slots, slot_stride, h_pairs, n_pairs, d_out, d_flags, s);
+  if (app->p.kind == RK_APP_GMM) return gmm_compare_list(app, d_slots, slot_stride, h_pairs, n_pairs, d_out, d_flags, s);
+  if (app->p.kind == RK_APP_CV) return cv_compare_list(app, d_slots, slot_stride, h_pairs, n_pairs, d_out, d_flags, s);
   const int lim = batch_limit(app);
   PairBatch b;
   for (int base = 0; base < n_pairs; base += lim) {
@@ -167,6 +168,8 @@ void rk_app_destroy(rk_app* app) {
   cudaSetDevice(app->device);
   if (app->p.kind == RK_APP_PCE) pce_free(app);
   if (app->p.kind == RK_APP_NCC) ncc_free(app);
+  delete app->job;
+  cudaFree(app->gmm_scratch);
   delete app;
 }
 

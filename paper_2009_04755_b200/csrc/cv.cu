@@ -84,49 +84,95 @@ __device__ __forceinline__ int merge_path(const uint64_t* a, int na, const uint6
   return lo;
 }
 
-// One warp per pair (8 pairs per CTA).
-__global__ void __launch_bounds__(256) cv_compare_kernel(PairBatch b, const uint8_t* __restrict__ slots,
-                                                         size_t slot_stride, int cap, double* __restrict__ out,
-                                                         uint8_t* __restrict__ flags, double threshold) {
+// One CTA (8 warps) per pair.  The merged sequence of the two sorted token
+// lists is split by merge path into 8 warp partitions; inside its partition a
+// warp walks both lists in coalesced 32-token windows: every lane binary-searches
+// its A token in the B window (register shuffles), matches add fa*fb (fp64, in
+// order), and the window whose last token is smaller is consumed whole while the
+// other advances by the ballot count of tokens below it.  A match is always
+// counted from the A side, so a B token just past the partition (equal to the
+// partition's last A token, ties go to A) is still found: the B window may read
+// beyond the partition's end.
+constexpr int kCvWarps = 8;
+
+__global__ void __launch_bounds__(kCvWarps * 32) cv_pair_kernel(const PceJob job, const uint8_t* __restrict__ slots,
+                                                                size_t slot_stride, int cap, double* __restrict__ out,
+                                                                uint8_t* __restrict__ flags, double threshold) {
+  __shared__ double s_dot[kCvWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * 8 + warp;
-  if (p >= b.npairs) return;
-  const uint8_t* sa = slots + (size_t)b.slot_a[p] * slot_stride;
-  const uint8_t* sb = slots + (size_t)b.slot_b[p] * slot_stride;
+  const DevPair pr = job.pairs[blockIdx.x];
+  const uint8_t* sa = slots + (size_t)pr.slot_a * slot_stride;
+  const uint8_t* sb = slots + (size_t)pr.slot_b * slot_stride;
   const int na = (int)*reinterpret_cast<const uint32_t*>(sa);
   const int nb = (int)*reinterpret_cast<const uint32_t*>(sb);
-  const double norm_a = *reinterpret_cast<const double*>(sa + 8);
-  const double norm_b = *reinterpret_cast<const double*>(sb + 8);
   const uint64_t* ta = reinterpret_cast<const uint64_t*>(sa + 16);
   const uint64_t* tb = reinterpret_cast<const uint64_t*>(sb + 16);
   const double* fa = reinterpret_cast<const double*>(sa + 16 + 8 * (size_t)cap);
   const double* fb = reinterpret_cast<const double*>(sb + 16 + 8 * (size_t)cap);
-  const int total = na + nb;
-  const int per = (total + 31) / 32;
-  const int d0 = min(total, lane * per), d1 = min(total, d0 + per);
+  const int64_t total = (int64_t)na + nb;
+  const int d0 = (int)(total * warp / kCvWarps), d1 = (int)(total * (warp + 1) / kCvWarps);
   int i = merge_path(ta, na, tb, nb, d0);
   int j = d0 - i;
   const int i_end = merge_path(ta, na, tb, nb, d1);
-  const int j_end = d1 - i_end;
+  constexpr uint64_t kInf = ~0ull;   // sentinel: k-mer ids of UTF-8 text never reach 2^64 - 1
+  auto lda = [&](int idx) { return idx < i_end ? __ldg(ta + idx) : kInf; };
+  auto ldb = [&](int idx) { return idx < nb ? __ldg(tb + idx) : kInf; };
+  // current windows (a, b) and the next ones (an, bn), loaded one iteration ahead
+  uint64_t a = lda(i + lane), an = lda(i + 32 + lane);
+  uint64_t b = ldb(j + lane), bn = ldb(j + 32 + lane);
   double dot = 0.0;
-  // Ties take A first, so when A[i] is consumed the B head is the only
-  // candidate match (tokens are unique and sorted within each item); the head
-  // may already belong to the next lane's segment, which is fine to read.
-  while (i < i_end || j < j_end) {
-    const bool take_a = (i < i_end) && (j >= j_end || ta[i] <= tb[j]);
-    if (take_a) {
-      if (j < nb && tb[j] == ta[i]) dot = fma(fa[i], fb[j], dot);
-      ++i;
+  while (i < i_end && j < nb) {
+    const int na_w = min(32, i_end - i);
+    const int nb_w = min(32, nb - j);
+    const uint64_t amax = __shfl_sync(0xffffffffu, a, na_w - 1);
+    const uint64_t bmax = __shfl_sync(0xffffffffu, b, nb_w - 1);
+    // lower_bound of a in the B window (lanes >= nb_w hold +inf)
+    int pos = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const uint64_t probe = __shfl_sync(0xffffffffu, b, pos + step - 1);
+      if (probe < a) pos += step;
+    }
+    const uint64_t at = __shfl_sync(0xffffffffu, b, pos & 31);
+    if (a != kInf && pos < nb_w && at == a) dot = fma(__ldg(fa + i + lane), __ldg(fb + j + pos), dot);
+    int adv_a, adv_b;
+    if (amax < bmax) {          // A window done; B tokens <= amax done too
+      adv_a = na_w;
+      adv_b = __popc(__ballot_sync(0xffffffffu, b <= amax));
+    } else if (bmax < amax) {   // B window done; A tokens <= bmax were checked against it
+      adv_b = nb_w;
+      adv_a = __popc(__ballot_sync(0xffffffffu, a <= bmax));
     } else {
-      ++j;
+      adv_a = na_w;
+      adv_b = nb_w;
+    }
+    if (adv_a) {   // slide the A window from (a, an), prefetch the next one
+      const int src = lane + adv_a;
+      const uint64_t x0 = __shfl_sync(0xffffffffu, a, src & 31), x1 = __shfl_sync(0xffffffffu, an, src & 31);
+      a = src < 32 ? x0 : x1;
+      i += adv_a;
+      an = lda(i + 32 + lane);
+    }
+    if (adv_b) {
+      const int src = lane + adv_b;
+      const uint64_t x0 = __shfl_sync(0xffffffffu, b, src & 31), x1 = __shfl_sync(0xffffffffu, bn, src & 31);
+      b = src < 32 ? x0 : x1;
+      j += adv_b;
+      bn = ldb(j + 32 + lane);
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  if (lane == 0) {
-    const double v = (norm_a > 0.0 && norm_b > 0.0) ? dot / (norm_a * norm_b) : 0.0;
-    out[b.pid[p]] = v;
-    if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
+  if (lane == 0) s_dot[warp] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kCvWarps; ++w) t += s_dot[w];
+    const double norm_a = *reinterpret_cast<const double*>(sa + 8);
+    const double norm_b = *reinterpret_cast<const double*>(sb + 8);
+    const double v = (norm_a > 0.0 && norm_b > 0.0) ? t / (norm_a * norm_b) : 0.0;
+    out[pr.pid] = v;
+    if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
   }
 }
 
@@ -166,12 +212,22 @@ rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
   return RK_OK;
 }
 
-rk_status cv_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
-                     uint8_t* d_flags, cudaStream_t s) {
-  cv_compare_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const uint8_t*>(d_slots), slot_stride,
-                                                       app->p.max_entries, d_out, d_flags, threshold_or_nan(app));
-  app->launches += 1;
-  RK_CUDA(cudaGetLastError());
+rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                         double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  if (!app->job) app->job = new PceJob();
+  PceJob& job = *app->job;
+  for (int base = 0; base < n; base += kPipeMaxPairs) {
+    const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
+    job.npairs = m;
+    for (int k = 0; k < m; ++k) {
+      const rk_pair& q = pairs[base + k];
+      job.pairs[k] = DevPair{q.slot_a, q.slot_b, pair_id(app->p.n, q.i, q.j)};
+    }
+    cv_pair_kernel<<<m, kCvWarps * 32, 0, s>>>(job, static_cast<const uint8_t*>(d_slots), slot_stride,
+                                               app->p.max_entries, d_out, d_flags, threshold_or_nan(app));
+    app->launches += 1;
+    RK_CUDA(cudaGetLastError());
+  }
   return RK_OK;
 }
 

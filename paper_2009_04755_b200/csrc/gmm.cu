@@ -9,8 +9,7 @@
 // fixed so the result is deterministic):
 //   E_k    = sum_a sum_b exp( -|R(theta_k) p_a - q_b|^2 / (s_a^2 + s_b^2 + s0) )
 //   value  = max_k E_k / (m_i * m_j)
-// One warp per pair: both particles staged in the warp's shared memory, lane
-// stripes over a, sequential over b (fixed order), warp tree reduction per k.
+// One CTA per pair (gmm_pair_kernel below), up to 1,024 pairs per launch.
 // Oracle: oracle/gmm.py (parity unpinned by the reference; 1e-4 relative).
 #include <math.h>
 
@@ -20,7 +19,6 @@ namespace rk {
 
 namespace {
 
-constexpr int kWarps = 4;   // pairs per CTA
 
 __global__ void gmm_preprocess_kernel(const uint8_t* __restrict__ parsed, size_t parsed_stride, SlotList dst,
                                       uint8_t* __restrict__ slots, size_t slot_stride, int cap,
@@ -58,53 +56,117 @@ __global__ void gmm_preprocess_kernel(const uint8_t* __restrict__ parsed, size_t
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) gmm_compare_kernel(PairBatch b, const uint8_t* __restrict__ slots,
-                                                                  size_t slot_stride, int cap, int angles, float s0,
-                                                                  double* __restrict__ out,
-                                                                  uint8_t* __restrict__ flags, double threshold) {
-  extern __shared__ float4 gsm[];
+// One CTA (8 warps) per pair.  Work units = (32-point chunk of particle i) x
+// (quarter of particle j), dealt round-robin to the warps; particle j sits in
+// shared memory as (x, y, s^2 + s0, |q|^2) and is read by broadcast.  The
+// rotation leaves |p| unchanged, so per (a, b, k)
+//   -|R_k p - q|^2 w = (2 (R_k p).q - |p|^2 - |q|^2) w,   w = log2(e) / (s_a^2 + s_b^2)
+// costs one FMUL + two FFMA + one MUFU.EX2 (+ the add): the reciprocal is shared
+// by the 12 angles of a block, so the kernel is bound by the SFU's ex2 rate.
+constexpr int kPairWarps = 8;
+constexpr int kAngBlock = 12;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// grid = pairs x angle blocks: CTA (p, ab) evaluates angles 12ab .. 12ab+11 of
+// pair p and stores its best E_k in blk_best[p * nblk + ab]; gmm_finalize takes
+// the max over the blocks (order-independent: deterministic).  Splitting the
+// angle grid over CTAs gives ~7 waves per 1,024-pair launch instead of 2.3.
+__global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PceJob job, const uint8_t* __restrict__ slots,
+                                                                   size_t slot_stride, int angles, float s0,
+                                                                   double* __restrict__ blk_best) {
+  extern __shared__ float4 Q[];                       // particle j (m_j entries)
+  __shared__ float2 s_cs[kAngBlock];                  // (cos, sin) of this CTA's angles
+  __shared__ float s_part[kPairWarps][kAngBlock];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kWarps + warp;
-  if (p >= b.npairs) return;
-  float4* P = gsm + (size_t)warp * 2 * cap;   // particle i: (x, y, s^2)
-  float4* Q = P + cap;                        // particle j
-  const uint8_t* si = slots + (size_t)b.slot_a[p] * slot_stride;
-  const uint8_t* sj = slots + (size_t)b.slot_b[p] * slot_stride;
+  const int nblk = (angles + kAngBlock - 1) / kAngBlock;
+  const int ab = blockIdx.x % nblk;
+  const DevPair pr = job.pairs[blockIdx.x / nblk];
+  const uint8_t* si = slots + (size_t)pr.slot_a * slot_stride;
+  const uint8_t* sj = slots + (size_t)pr.slot_b * slot_stride;
   const int mi = (int)*reinterpret_cast<const uint32_t*>(si);
   const int mj = (int)*reinterpret_cast<const uint32_t*>(sj);
   const float* pi = reinterpret_cast<const float*>(si + 8);
   const float* pj = reinterpret_cast<const float*>(sj + 8);
-  for (int a = lane; a < mi; a += 32) P[a] = make_float4(pi[3 * a], pi[3 * a + 1], pi[3 * a + 2], 0.f);
-  for (int c = lane; c < mj; c += 32) Q[c] = make_float4(pj[3 * c], pj[3 * c + 1], pj[3 * c + 2] + s0, 0.f);
-  __syncwarp();
-  constexpr float kLog2e = 1.4426950408889634f;
-  double best = -1.0;
-  for (int k = 0; k < angles; ++k) {
+  for (int c = threadIdx.x; c < mj; c += blockDim.x) {
+    const float x = pj[3 * c], y = pj[3 * c + 1];
+    Q[c] = make_float4(x, y, pj[3 * c + 2] + s0, fmaf(x, x, y * y));
+  }
+  for (int t = threadIdx.x; t < kAngBlock; t += blockDim.x) {
+    const int k = min(ab * kAngBlock + t, angles - 1);   // pad the last block with a repeated angle
     float sn, cs;
     sincospif(2.0f * (float)k / (float)angles, &sn, &cs);
-    float acc = 0.f;
-    for (int a = lane; a < mi; a += 32) {
-      const float4 u = P[a];
-      const float rx = cs * u.x - sn * u.y, ry = sn * u.x + cs * u.y;
-      float part = 0.f;
-      for (int c = 0; c < mj; ++c) {
-        const float4 v = Q[c];
-        const float dx = rx - v.x, dy = ry - v.y;
-        const float d2 = fmaf(dx, dx, dy * dy);
-        part += exp2f(-kLog2e * d2 / (u.z + v.z));
-      }
-      acc += part;
-    }
-    double e = (double)acc;
+    s_cs[t] = make_float2(cs, sn);
+  }
+  __syncthreads();
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int n_chunks = (mi + 31) / 32;
+  const int units = n_chunks * 4;
+  const int qlen = (mj + 3) / 4;
+  {
+    float acc[kAngBlock];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    best = fmax(best, e);
+    for (int t = 0; t < kAngBlock; ++t) acc[t] = 0.f;
+    for (int u = warp; u < units; u += kPairWarps) {
+      const int a = (u >> 2) * 32 + lane;
+      const int c0 = (u & 3) * qlen, c1 = min(mj, c0 + qlen);
+      if (a < mi) {
+        const float px = pi[3 * a], py = pi[3 * a + 1], sa = pi[3 * a + 2];
+        const float pp = fmaf(px, px, py * py);
+        float rx[kAngBlock], ry[kAngBlock];
+#pragma unroll
+        for (int t = 0; t < kAngBlock; ++t) {
+          const float2 w = s_cs[t];
+          rx[t] = w.x * px - w.y * py;
+          ry[t] = w.y * px + w.x * py;
+        }
+        for (int c = c0; c < c1; ++c) {
+          const float4 q = Q[c];
+          const float w = __fdividef(kLog2e, sa + q.z);
+          const float w2 = 2.0f * w;
+          const float base = -(pp + q.w) * w;
+#pragma unroll
+          for (int t = 0; t < kAngBlock; ++t) {
+            const float dot = fmaf(rx[t], q.x, ry[t] * q.y);
+            acc[t] += ex2_approx(fmaf(dot, w2, base));
+          }
+        }
+      }
+    }
+    // warp sums, then a fixed-order sum over the warps
+#pragma unroll
+    for (int t = 0; t < kAngBlock; ++t) {
+      float v = acc[t];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s_part[warp][t] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double best = -1.0;
+      for (int t = 0; t < kAngBlock; ++t) {
+        double e = 0.0;
+        for (int w = 0; w < kPairWarps; ++w) e += (double)s_part[w][t];
+        best = fmax(best, e);
+      }
+      blk_best[blockIdx.x] = best / ((double)mi * (double)mj);
+    }
   }
-  if (lane == 0) {
-    const double v = best / ((double)mi * (double)mj);
-    out[b.pid[p]] = v;
-    if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
-  }
+}
+
+__global__ void gmm_finalize(const PceJob job, int nblk, const double* __restrict__ blk_best,
+                             double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= job.npairs) return;
+  double v = -1.0;
+  for (int b = 0; b < nblk; ++b) v = fmax(v, blk_best[(size_t)p * nblk + b]);
+  const int64_t pid = job.pairs[p].pid;
+  out[pid] = v;
+  if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
 }
 
 }  // namespace
@@ -115,9 +177,13 @@ rk_status gmm_init(rk_app* app) {
   if (app->p.gmm_angles <= 0) app->p.gmm_angles = 36;
   app->slot_bytes = 8 + 12 * (size_t)cap;
   app->parsed_bytes = 8 + 12 * (size_t)cap;
-  const size_t smem = (size_t)kWarps * 2 * cap * sizeof(float4);
+  if (app->p.gmm_angles > 256) return set_error(RK_ERR_UNSUPPORTED, "GMM angle grid > 256");
+  const size_t smem = (size_t)cap * sizeof(float4);
   if (smem > 200 * 1024) return set_error(RK_ERR_UNSUPPORTED, "GMM max_entries %d too large for shared memory", cap);
-  RK_CUDA(cudaFuncSetAttribute(gmm_compare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RK_CUDA(cudaFuncSetAttribute(gmm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!app->job) app->job = new PceJob();
+  const int nblk = (app->p.gmm_angles + kAngBlock - 1) / kAngBlock;
+  RK_CUDA(cudaMalloc(&app->gmm_scratch, sizeof(double) * kPipeMaxPairs * nblk));
   return RK_OK;
 }
 
@@ -147,14 +213,24 @@ rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
   return RK_OK;
 }
 
-rk_status gmm_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
-                      uint8_t* d_flags, cudaStream_t s) {
-  const size_t smem = (size_t)kWarps * 2 * app->p.max_entries * sizeof(float4);
-  gmm_compare_kernel<<<(b.npairs + kWarps - 1) / kWarps, kWarps * 32, smem, s>>>(
-      b, static_cast<const uint8_t*>(d_slots), slot_stride, app->p.max_entries, app->p.gmm_angles, app->p.gmm_scale,
-      d_out, d_flags, threshold_or_nan(app));
-  app->launches += 1;
-  RK_CUDA(cudaGetLastError());
+rk_status gmm_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                          double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  const size_t smem = (size_t)app->p.max_entries * sizeof(float4);
+  PceJob& job = *app->job;
+  for (int base = 0; base < n; base += kPipeMaxPairs) {
+    const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
+    job.npairs = m;
+    for (int k = 0; k < m; ++k) {
+      const rk_pair& q = pairs[base + k];
+      job.pairs[k] = DevPair{q.slot_a, q.slot_b, pair_id(app->p.n, q.i, q.j)};
+    }
+    const int nblk = (app->p.gmm_angles + kAngBlock - 1) / kAngBlock;
+    gmm_pair_kernel<<<m * nblk, kPairWarps * 32, smem, s>>>(job, static_cast<const uint8_t*>(d_slots), slot_stride,
+                                                            app->p.gmm_angles, app->p.gmm_scale, app->gmm_scratch);
+    gmm_finalize<<<(m + 127) / 128, 128, 0, s>>>(job, nblk, app->gmm_scratch, d_out, d_flags, threshold_or_nan(app));
+    app->launches += 2;
+    RK_CUDA(cudaGetLastError());
+  }
   return RK_OK;
 }
 

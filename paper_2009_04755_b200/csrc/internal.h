@@ -88,6 +88,8 @@ struct rk_app {
   size_t parsed_bytes = 0;
   int64_t launches = 0;    // kernels launched through this app (for bench accounting)
   int32_t slot_group = 1;  // slots interleaved in groups of this many (rk_app_slot_group)
+  rk::PceJob* job = nullptr;   // host staging of by-value pair lists (GMM, CV launches)
+  double* gmm_scratch = nullptr;   // per (pair, angle block) best of one GMM launch
   rk::PceState pce;
   rk::NccState ncc;
 };
@@ -120,8 +122,8 @@ rk_status synth_compare(rk_app* app, const PairBatch& b, double* d_out, uint8_t*
 rk_status gmm_init(rk_app* app);
 rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                          size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s);
-rk_status gmm_compare(rk_app* app, const void* d_slots, size_t slot_stride, const PairBatch& b, double* d_out,
-                      uint8_t* d_flags, cudaStream_t s);
+rk_status gmm_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
+                          double* d_out, uint8_t* d_flags, cudaStream_t s);
 rk_status ncc_init(rk_app* app);
 void ncc_free(rk_app* app);
 rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,

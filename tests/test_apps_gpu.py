@@ -185,3 +185,51 @@ def test_allpairs_engine_public_api(tmp_path):
     assert r.left == 2 and r.right == 5 and r.match == (2 % 3 == 5 % 3)
     assert len(res.results()) == 45
     eng.close()
+
+
+def test_cv_large_skewed_items_match_oracle():
+    """Windowed merge over long, skewed token lists: sizes 1 .. 60k, identical,
+    disjoint, nested and heavily overlapping items, matches straddling the warp
+    partitions; against the oracle's sequential merge (oracle/cv.py) at 1e-12."""
+    from oracle import cv as ocv
+    _l, device = _mods()
+    rng = np.random.default_rng(5)
+    pool = np.unique(rng.integers(1, 1 << 40, size=200_000).astype(np.uint64))
+    sizes = [1, 2, 31, 33, 1000, 60_000, 60_000, 45_000, 5_000, 20_000, 7]
+    toks = []
+    for k, m in enumerate(sizes):
+        if k == 6:
+            t = toks[5]                                   # identical to item 5
+        elif k == 7:
+            t = np.sort(rng.choice(toks[5], size=m, replace=False))   # nested in item 5
+        elif k == 8:
+            t = np.unique(rng.integers(1 << 41, 1 << 42, size=m).astype(np.uint64))   # disjoint range
+        else:
+            t = np.sort(rng.choice(pool, size=m, replace=False))
+        toks.append(t)
+    n, cap = len(toks), max(len(t) for t in toks)
+    stride = 4 + 12 * cap
+    buf = np.zeros((n, stride), dtype=np.uint8)
+    vecs = []
+    counts = []
+    for k, t in enumerate(toks):
+        cnt = counts[5] if k == 6 else rng.integers(1, 9, size=len(t)).astype(np.uint32)
+        counts.append(cnt)
+        rec = np.zeros(len(t), dtype=[("t", "<u8"), ("c", "<u4")])
+        rec["t"], rec["c"] = t, cnt
+        blob = struct.pack("<I", len(t)) + rec.tobytes()
+        buf[k, :len(blob)] = np.frombuffer(blob, dtype=np.uint8)
+        vecs.append(ocv.preprocess(blob))
+    app = device.DeviceApp(_l.app_params(_l.APP_CV, n, max_entries=cap, threshold=0.5))
+    slots = app.alloc_slots(n)
+    app.preprocess(torch.from_numpy(buf.reshape(-1)).cuda(), stride, n, slots, list(range(n)))
+    out = torch.zeros(n * (n - 1) // 2, dtype=torch.float64, device="cuda")
+    app.compare_tile(slots, 0, n, 0, n, list(range(n)), out)
+    got = out.cpu().numpy()
+    pid = 0
+    for i in range(n):
+        for j in range(i + 1, n):
+            want = ocv.compare(vecs[i], vecs[j])
+            assert abs(got[pid] - want) <= 1e-12 * max(1.0, abs(want)), (i, j, got[pid], want)
+            pid += 1
+    assert got[5 * (2 * n - 5 - 1) // 2 + 0] == pytest.approx(1.0, abs=1e-12)   # identical items 5, 6

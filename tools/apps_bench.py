@@ -1,0 +1,150 @@
+"""Throughput of the irregular apps at their BASELINE configs on one B200.
+
+  python tools/apps_bench.py gmm [--items 1000] [--angles 36]     # configs[3] (C4)
+  python tools/apps_bench.py cv  [--items 2500] [--mean-nnz 500000] # configs[4] (C5), one GPU
+
+GMM: N particles of ~300 localizations (synthdata.particle), max over K
+rotations of the Gaussian-overlap cost; bound = SFU exponentials, K*m_i*m_j per
+pair, against 148 SMs x 16 ex2/clk x clock.
+CV: N sparse k-mer composition vectors with log-normally skewed nnz in
+[1e5, 1.8e6], generated directly in the reference's parsed byte
+format (<I dim> + dim x <Q token><I count>); bound = HBM, 16*(nnz_i + nnz_j)
+bytes per pair.  Items are HBM-resident before the timed region; one step = the
+whole all-pairs job through the C++ engine (preprocess + every pair).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2009_04755_b200 import _lib, device  # noqa: E402
+
+
+def run_engine(params, parsed, stride: int, n: int, leaf: int, steps: int, warmup: int):
+    items = parsed if isinstance(parsed, torch.Tensor) else torch.from_numpy(parsed).cuda()
+    eng = device.DeviceEngine(params, leaf_block=leaf, device_slots=n)
+    total = n * (n - 1) // 2
+    out = torch.zeros(total, dtype=torch.float64, device="cuda")
+    estream = torch.cuda.ExternalStream(eng.stream())
+    for _ in range(warmup):
+        eng.run(out, device_items=items, parsed_stride=stride)
+    eng.reset_stats()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(estream)
+    for _ in range(steps):
+        eng.run(out, device_items=items, parsed_stride=stride)
+    e1.record(estream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    st = eng.stats()
+    eng.close()
+    return ms, st, out
+
+
+def bench_gmm(args):
+    from paper_2009_04755_b200.synthdata import particle
+    n, maxp = args.items, 400
+    stride = 8 + 12 * maxp
+    host = np.zeros((n, stride), dtype=np.uint8)
+    msum = np.zeros(n)
+    for k in range(n):
+        p = particle(k, args.seed)
+        msum[k] = len(p)
+        host[k, :8] = np.frombuffer(np.array([len(p), 0], dtype="<u4").tobytes(), dtype=np.uint8)
+        host[k, 8:8 + 12 * len(p)] = np.frombuffer(p.astype("<f4").tobytes(), dtype=np.uint8)
+    params = _lib.app_params(_lib.APP_GMM, n, max_entries=maxp, gmm_angles=args.angles)
+    ms, st, _ = run_engine(params, host.reshape(-1), stride, n, args.leaf, args.steps, args.warmup)
+    pairs = n * (n - 1) // 2
+    exps = args.angles * (msum.sum() ** 2 - (msum ** 2).sum()) / 2.0
+    clk_ghz = args.clock_ghz
+    sfu_peak = 148 * 16 * clk_ghz * 1e9
+    return {"app": "gmm", "workload": f"particle fusion, N={n} particles of ~300 localizations, K={args.angles} "
+                                      f"rotations (BASELINE configs[3])",
+            "pairs": pairs, "ms_per_job": ms, "pairs_per_s": pairs / (ms / 1e3),
+            "roofline": {"bound": "sfu", "achieved_exp_per_s": exps / (ms / 1e3), "peak_exp_per_s": sfu_peak,
+                         "frac": exps / (ms / 1e3) / sfu_peak, "exps_per_job": exps,
+                         "peak_source": f"148 SMs x 16 ex2/clk x {clk_ghz} GHz"},
+            "launches": st["kernel_launches"]}
+
+
+def cv_items(n: int, mean_nnz: float, seed: int, vocab_bits: int = 26):
+    """Sparse composition vectors in the reference's parsed format, skewed nnz,
+    generated on the device (torch) straight into the parsed buffer."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    nnz = np.clip(rng.lognormal(np.log(mean_nnz), 0.6, size=n), 1e5, 1.8e6).astype(np.int64)
+    cap = int(nnz.max())
+    stride = (4 + 12 * cap + 15) // 16 * 16
+    buf = torch.zeros(n * stride, dtype=torch.uint8, device="cuda")
+    pools = {}
+    for k in range(n):
+        fam = k % 16
+        if fam not in pools:   # a family's shared token pool -> non-trivial cosines
+            pools[fam] = torch.randint(0, 1 << vocab_bits, (2_000_000,), generator=g, device="cuda")
+        m = int(nnz[k])
+        shared = pools[fam][torch.randint(0, 2_000_000, (m // 2,), generator=g, device="cuda")]
+        own = torch.randint(0, 1 << vocab_bits, (m - m // 2,), generator=g, device="cuda")
+        tok = torch.unique(torch.cat([shared, own]))          # sorted, unique
+        cnt = torch.randint(1, 50, (tok.numel(),), generator=g, device="cuda", dtype=torch.int32)
+        rec = torch.cat([tok.view(torch.uint8).view(-1, 8), cnt.view(torch.uint8).view(-1, 4)], dim=1).reshape(-1)
+        base = k * stride
+        buf[base:base + 4] = torch.tensor([tok.numel()], dtype=torch.int32, device="cuda").view(torch.uint8)
+        buf[base + 4:base + 4 + rec.numel()] = rec
+        nnz[k] = tok.numel()
+    torch.cuda.synchronize()
+    return buf, stride, cap, nnz
+
+
+def bench_cv(args):
+    n = args.items
+    buf, stride, cap, nnz = cv_items(n, args.mean_nnz, args.seed)
+    params = _lib.app_params(_lib.APP_CV, n, max_entries=cap, threshold=0.5)
+    ms, st, _ = run_engine(params, buf, stride, n, args.leaf, args.steps, args.warmup)
+    pairs = n * (n - 1) // 2
+    alg = 16.0 * (n - 1) * nnz.sum()        # sum over pairs of 16 (nnz_i + nnz_j)
+    hbm = 6544.3
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm = float(json.load(fh).get("hbm_gbs", hbm))
+    except Exception:
+        pass
+    return {"app": "cv", "workload": f"composition-vector cosine, N={n} items, nnz lognormal in [1e5, 1.8e6] "
+                                     f"(mean {nnz.mean():.0f}, max {nnz.max()}) (BASELINE configs[4], 1 GPU)",
+            "pairs": pairs, "ms_per_job": ms, "pairs_per_s": pairs / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved_gbs": alg / (ms / 1e3) / 1e9, "peak_gbs": hbm,
+                         "frac": alg / (ms / 1e3) / 1e9 / hbm, "alg_bytes_per_job": alg},
+            "launches": st["kernel_launches"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("app", choices=["gmm", "cv"])
+    ap.add_argument("--items", type=int, default=0)
+    ap.add_argument("--angles", type=int, default=36)
+    ap.add_argument("--mean-nnz", type=float, default=5e5)
+    ap.add_argument("--leaf", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--clock-ghz", type=float, default=1.965)
+    args = ap.parse_args()
+    if args.app == "gmm":
+        args.items = args.items or 1000
+        print(json.dumps(bench_gmm(args)), flush=True)
+    else:
+        args.items = args.items or 2500
+        print(json.dumps(bench_cv(args)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
