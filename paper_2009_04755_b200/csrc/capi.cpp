@@ -170,6 +170,7 @@ void rk_app_destroy(rk_app* app) {
   if (app->p.kind == RK_APP_NCC) ncc_free(app);
   delete app->job;
   cudaFree(app->gmm_scratch);
+  cudaFree(app->cv_scratch);
   delete app;
 }
 

@@ -12,6 +12,8 @@
 // Slot layout (device):  u32 dim | u32 pad | f64 norm | u64 token[cap] | f64 freq[cap]
 #include <math.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace rk {
@@ -84,96 +86,175 @@ __device__ __forceinline__ int merge_path(const uint64_t* a, int na, const uint6
   return lo;
 }
 
-// One CTA (8 warps) per pair.  The merged sequence of the two sorted token
-// lists is split by merge path into 8 warp partitions; inside its partition a
-// warp walks both lists in coalesced 32-token windows: every lane binary-searches
-// its A token in the B window (register shuffles), matches add fa*fb (fp64, in
-// order), and the window whose last token is smaller is consumed whole while the
-// other advances by the ballot count of tokens below it.  A match is always
-// counted from the A side, so a B token just past the partition (equal to the
-// partition's last A token, ties go to A) is still found: the B window may read
-// beyond the partition's end.
+// Work is split into units of ~kUnit merged tokens: pair p gets Q_p =
+// ceil((na + nb) / kUnit) units (diagonals of its merge path), so the skewed
+// sizes of C5 (1e5 .. 1.8e6 tokens) cost proportionally and the launch has no
+// per-pair tail.  cv_units sizes and scans them, persistent warps of cv_work
+// grab units from an atomic counter, cv_finalize sums each pair's unit partials
+// in unit order (deterministic) and writes the cosine.
+//
+// Inside a unit the warp walks both lists in coalesced 32-token windows: every
+// lane binary-searches its A token in the B window (register shuffles), matches
+// add fa*fb (fp64, in order), and the window whose last token is smaller is
+// consumed whole while the other advances by the ballot count of tokens below
+// it; the next windows are loaded one step ahead.  A match is always counted
+// from the A side, so a B token just past the unit (equal to the unit's last A
+// token, ties go to A) is still found: the B window may read beyond the unit.
 constexpr int kCvWarps = 8;
+constexpr int kUnit = 32768;
+constexpr int kMaxUnits = 64;      // per pair (larger pairs get larger units)
 
-__global__ void __launch_bounds__(kCvWarps * 32) cv_pair_kernel(const PceJob job, const uint8_t* __restrict__ slots,
-                                                                size_t slot_stride, int cap, double* __restrict__ out,
-                                                                uint8_t* __restrict__ flags, double threshold) {
-  __shared__ double s_dot[kCvWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DevPair pr = job.pairs[blockIdx.x];
+struct CvPairRef {
+  const uint64_t* ta;
+  const uint64_t* tb;
+  const double* fa;
+  const double* fb;
+  int na, nb;
+};
+
+__device__ __forceinline__ CvPairRef cv_pair_ref(const DevPair& pr, const uint8_t* slots, size_t slot_stride, int cap) {
   const uint8_t* sa = slots + (size_t)pr.slot_a * slot_stride;
   const uint8_t* sb = slots + (size_t)pr.slot_b * slot_stride;
-  const int na = (int)*reinterpret_cast<const uint32_t*>(sa);
-  const int nb = (int)*reinterpret_cast<const uint32_t*>(sb);
-  const uint64_t* ta = reinterpret_cast<const uint64_t*>(sa + 16);
-  const uint64_t* tb = reinterpret_cast<const uint64_t*>(sb + 16);
-  const double* fa = reinterpret_cast<const double*>(sa + 16 + 8 * (size_t)cap);
-  const double* fb = reinterpret_cast<const double*>(sb + 16 + 8 * (size_t)cap);
-  const int64_t total = (int64_t)na + nb;
-  const int d0 = (int)(total * warp / kCvWarps), d1 = (int)(total * (warp + 1) / kCvWarps);
-  int i = merge_path(ta, na, tb, nb, d0);
-  int j = d0 - i;
-  const int i_end = merge_path(ta, na, tb, nb, d1);
-  constexpr uint64_t kInf = ~0ull;   // sentinel: k-mer ids of UTF-8 text never reach 2^64 - 1
-  auto lda = [&](int idx) { return idx < i_end ? __ldg(ta + idx) : kInf; };
-  auto ldb = [&](int idx) { return idx < nb ? __ldg(tb + idx) : kInf; };
-  // current windows (a, b) and the next ones (an, bn), loaded one iteration ahead
-  uint64_t a = lda(i + lane), an = lda(i + 32 + lane);
-  uint64_t b = ldb(j + lane), bn = ldb(j + 32 + lane);
-  double dot = 0.0;
-  while (i < i_end && j < nb) {
-    const int na_w = min(32, i_end - i);
-    const int nb_w = min(32, nb - j);
-    const uint64_t amax = __shfl_sync(0xffffffffu, a, na_w - 1);
-    const uint64_t bmax = __shfl_sync(0xffffffffu, b, nb_w - 1);
-    // lower_bound of a in the B window (lanes >= nb_w hold +inf)
-    int pos = 0;
-#pragma unroll
-    for (int step = 16; step; step >>= 1) {
-      const uint64_t probe = __shfl_sync(0xffffffffu, b, pos + step - 1);
-      if (probe < a) pos += step;
-    }
-    const uint64_t at = __shfl_sync(0xffffffffu, b, pos & 31);
-    if (a != kInf && pos < nb_w && at == a) dot = fma(__ldg(fa + i + lane), __ldg(fb + j + pos), dot);
-    int adv_a, adv_b;
-    if (amax < bmax) {          // A window done; B tokens <= amax done too
-      adv_a = na_w;
-      adv_b = __popc(__ballot_sync(0xffffffffu, b <= amax));
-    } else if (bmax < amax) {   // B window done; A tokens <= bmax were checked against it
-      adv_b = nb_w;
-      adv_a = __popc(__ballot_sync(0xffffffffu, a <= bmax));
-    } else {
-      adv_a = na_w;
-      adv_b = nb_w;
-    }
-    if (adv_a) {   // slide the A window from (a, an), prefetch the next one
-      const int src = lane + adv_a;
-      const uint64_t x0 = __shfl_sync(0xffffffffu, a, src & 31), x1 = __shfl_sync(0xffffffffu, an, src & 31);
-      a = src < 32 ? x0 : x1;
-      i += adv_a;
-      an = lda(i + 32 + lane);
-    }
-    if (adv_b) {
-      const int src = lane + adv_b;
-      const uint64_t x0 = __shfl_sync(0xffffffffu, b, src & 31), x1 = __shfl_sync(0xffffffffu, bn, src & 31);
-      b = src < 32 ? x0 : x1;
-      j += adv_b;
-      bn = ldb(j + 32 + lane);
-    }
+  CvPairRef r;
+  r.na = (int)*reinterpret_cast<const uint32_t*>(sa);
+  r.nb = (int)*reinterpret_cast<const uint32_t*>(sb);
+  r.ta = reinterpret_cast<const uint64_t*>(sa + 16);
+  r.tb = reinterpret_cast<const uint64_t*>(sb + 16);
+  r.fa = reinterpret_cast<const double*>(sa + 16 + 8 * (size_t)cap);
+  r.fb = reinterpret_cast<const double*>(sb + 16 + 8 * (size_t)cap);
+  return r;
+}
+
+__device__ __forceinline__ int cv_units_of(int na, int nb) {
+  const int64_t t = (int64_t)na + nb;
+  const int64_t q = (t + kUnit - 1) / kUnit;
+  return q < 1 ? 1 : (q > kMaxUnits ? kMaxUnits : (int)q);
+}
+
+// one CTA of 1024 threads: unit offsets (exclusive scan), total, counter reset
+__global__ void __launch_bounds__(1024) cv_units(const PceJob job, const uint8_t* __restrict__ slots,
+                                                 size_t slot_stride, int* __restrict__ offsets,
+                                                 int* __restrict__ ctl) {
+  __shared__ int s_scan[1024];
+  const int p = threadIdx.x;
+  int q = 0;
+  if (p < job.npairs) {
+    const uint8_t* sa = slots + (size_t)job.pairs[p].slot_a * slot_stride;
+    const uint8_t* sb = slots + (size_t)job.pairs[p].slot_b * slot_stride;
+    q = cv_units_of((int)*reinterpret_cast<const uint32_t*>(sa), (int)*reinterpret_cast<const uint32_t*>(sb));
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  if (lane == 0) s_dot[warp] = dot;
+  s_scan[p] = q;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kCvWarps; ++w) t += s_dot[w];
-    const double norm_a = *reinterpret_cast<const double*>(sa + 8);
-    const double norm_b = *reinterpret_cast<const double*>(sb + 8);
-    const double v = (norm_a > 0.0 && norm_b > 0.0) ? t / (norm_a * norm_b) : 0.0;
-    out[pr.pid] = v;
-    if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
+  for (int o = 1; o < 1024; o <<= 1) {   // Hillis-Steele inclusive scan
+    const int v = p >= o ? s_scan[p - o] : 0;
+    __syncthreads();
+    s_scan[p] += v;
+    __syncthreads();
   }
+  offsets[p + 1] = s_scan[p];
+  if (p == 0) {
+    offsets[0] = 0;
+    ctl[0] = 0;                 // work counter
+    ctl[1] = s_scan[1023];      // total units
+  }
+}
+
+__global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PceJob job, const uint8_t* __restrict__ slots,
+                                                         size_t slot_stride, int cap, const int* __restrict__ offsets,
+                                                         int* __restrict__ ctl, double* __restrict__ partial) {
+  __shared__ int s_off[1025];
+  for (int k = threadIdx.x; k <= job.npairs; k += blockDim.x) s_off[k] = offsets[k];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int total_units = ctl[1];
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(&ctl[0], 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= total_units) break;
+    int lo = 0, hi = job.npairs;            // pair p: s_off[p] <= u < s_off[p + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= u) lo = mid;
+      else hi = mid;
+    }
+    const int p = lo, q = u - s_off[p], nq = s_off[p + 1] - s_off[p];
+    const CvPairRef r = cv_pair_ref(job.pairs[p], slots, slot_stride, cap);
+    const uint64_t* ta = r.ta;
+    const uint64_t* tb = r.tb;
+    const double* fa = r.fa;
+    const double* fb = r.fb;
+    const int na = r.na, nb = r.nb;
+    const int64_t tot = (int64_t)na + nb;
+    const int d0 = (int)(tot * q / nq), d1 = (int)(tot * (q + 1) / nq);
+    int i = merge_path(ta, na, tb, nb, d0);
+    int j = d0 - i;
+    const int i_end = merge_path(ta, na, tb, nb, d1);
+  constexpr uint64_t kInf = ~0ull;   // sentinel: k-mer ids of UTF-8 text never reach 2^64 - 1
+    auto lda = [&](int idx) { return idx < i_end ? __ldg(ta + idx) : kInf; };
+    auto ldb = [&](int idx) { return idx < nb ? __ldg(tb + idx) : kInf; };
+    // current windows (a, b) and the next ones (an, bn), loaded one iteration ahead
+    uint64_t a = lda(i + lane), an = lda(i + 32 + lane);
+    uint64_t b = ldb(j + lane), bn = ldb(j + 32 + lane);
+    double dot = 0.0;
+    while (i < i_end && j < nb) {
+      const int na_w = min(32, i_end - i);
+      const int nb_w = min(32, nb - j);
+      const uint64_t amax = __shfl_sync(0xffffffffu, a, na_w - 1);
+      const uint64_t bmax = __shfl_sync(0xffffffffu, b, nb_w - 1);
+      // lower_bound of a in the B window (lanes >= nb_w hold +inf)
+      int pos = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint64_t probe = __shfl_sync(0xffffffffu, b, pos + step - 1);
+        if (probe < a) pos += step;
+      }
+      const uint64_t at = __shfl_sync(0xffffffffu, b, pos & 31);
+      if (a != kInf && pos < nb_w && at == a) dot = fma(__ldg(fa + i + lane), __ldg(fb + j + pos), dot);
+      int adv_a, adv_b;
+      if (amax < bmax) {          // A window done; B tokens <= amax done too
+        adv_a = na_w;
+        adv_b = __popc(__ballot_sync(0xffffffffu, b <= amax));
+      } else if (bmax < amax) {   // B window done; A tokens <= bmax were checked against it
+        adv_b = nb_w;
+        adv_a = __popc(__ballot_sync(0xffffffffu, a <= bmax));
+      } else {
+        adv_a = na_w;
+        adv_b = nb_w;
+      }
+      if (adv_a) {   // slide the A window from (a, an), prefetch the next one
+        const int src = lane + adv_a;
+        const uint64_t x0 = __shfl_sync(0xffffffffu, a, src & 31), x1 = __shfl_sync(0xffffffffu, an, src & 31);
+        a = src < 32 ? x0 : x1;
+        i += adv_a;
+        an = lda(i + 32 + lane);
+      }
+      if (adv_b) {
+        const int src = lane + adv_b;
+        const uint64_t x0 = __shfl_sync(0xffffffffu, b, src & 31), x1 = __shfl_sync(0xffffffffu, bn, src & 31);
+        b = src < 32 ? x0 : x1;
+        j += adv_b;
+        bn = ldb(j + 32 + lane);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) partial[u] = dot;
+  }
+}
+
+__global__ void cv_finalize(const PceJob job, const uint8_t* __restrict__ slots, size_t slot_stride,
+                            const int* __restrict__ offsets, const double* __restrict__ partial,
+                            double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= job.npairs) return;
+  double t = 0.0;
+  for (int u = offsets[p]; u < offsets[p + 1]; ++u) t += partial[u];
+  const double norm_a = *reinterpret_cast<const double*>(slots + (size_t)job.pairs[p].slot_a * slot_stride + 8);
+  const double norm_b = *reinterpret_cast<const double*>(slots + (size_t)job.pairs[p].slot_b * slot_stride + 8);
+  const double v = (norm_a > 0.0 && norm_b > 0.0) ? t / (norm_a * norm_b) : 0.0;
+  out[job.pairs[p].pid] = v;
+  if (flags) flags[job.pairs[p].pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
 }
 
 }  // namespace
@@ -215,6 +296,19 @@ rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
 rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                          double* d_out, uint8_t* d_flags, cudaStream_t s) {
   if (!app->job) app->job = new PceJob();
+  if (!app->cv_scratch) {
+    // offsets [1025] | ctl [2] | partials [1024 * kMaxUnits]
+    RK_CUDA(cudaMalloc(&app->cv_scratch, sizeof(int) * 1028 + sizeof(double) * kPipeMaxPairs * kMaxUnits));
+    int dev = 0, sms = 0, per_sm = 0;
+    RK_CUDA(cudaGetDevice(&dev));
+    RK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cv_work, kCvWarps * 32, 0));
+    app->cv_grid = sms * std::max(1, per_sm);
+  }
+  int* offsets = static_cast<int*>(app->cv_scratch);
+  int* ctl = offsets + 1025;
+  double* partial = reinterpret_cast<double*>(static_cast<char*>(app->cv_scratch) + sizeof(int) * 1028);
+  const uint8_t* slots = static_cast<const uint8_t*>(d_slots);
   PceJob& job = *app->job;
   for (int base = 0; base < n; base += kPipeMaxPairs) {
     const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
@@ -223,9 +317,12 @@ rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, 
       const rk_pair& q = pairs[base + k];
       job.pairs[k] = DevPair{q.slot_a, q.slot_b, pair_id(app->p.n, q.i, q.j)};
     }
-    cv_pair_kernel<<<m, kCvWarps * 32, 0, s>>>(job, static_cast<const uint8_t*>(d_slots), slot_stride,
-                                               app->p.max_entries, d_out, d_flags, threshold_or_nan(app));
-    app->launches += 1;
+    cv_units<<<1, 1024, 0, s>>>(job, slots, slot_stride, offsets, ctl);
+    cv_work<<<app->cv_grid, kCvWarps * 32, 0, s>>>(job, slots, slot_stride, app->p.max_entries, offsets, ctl,
+                                                   partial);
+    cv_finalize<<<(m + 127) / 128, 128, 0, s>>>(job, slots, slot_stride, offsets, partial, d_out, d_flags,
+                                                threshold_or_nan(app));
+    app->launches += 3;
     RK_CUDA(cudaGetLastError());
   }
   return RK_OK;

@@ -90,6 +90,8 @@ struct rk_app {
   int32_t slot_group = 1;  // slots interleaved in groups of this many (rk_app_slot_group)
   rk::PceJob* job = nullptr;   // host staging of by-value pair lists (GMM, CV launches)
   double* gmm_scratch = nullptr;   // per (pair, angle block) best of one GMM launch
+  void* cv_scratch = nullptr;       // CV unit offsets, work counter and unit partials
+  int cv_grid = 0;                  // persistent CV work grid (SMs x resident CTAs)
   rk::PceState pce;
   rk::NccState ncc;
 };
