@@ -1,7 +1,8 @@
 """Throughput of the irregular apps at their BASELINE configs on one B200.
 
   python tools/apps_bench.py gmm [--items 1000] [--angles 36]     # configs[3] (C4)
-  python tools/apps_bench.py cv  [--items 2500] [--mean-nnz 500000] # configs[4] (C5), one GPU
+  python tools/apps_bench.py cv  [--items 2500] [--mean-nnz 500000] # configs[4] (C5)
+  (multi-GPU: python -m torch.distributed.run --nproc-per-node N ... tools/apps_bench.py cv)
 
 GMM: N particles of ~300 localizations (synthdata.particle), max over K
 rotations of the Gaussian-overlap cost; bound = SFU exponentials, K*m_i*m_j per
@@ -30,23 +31,62 @@ from paper_2009_04755_b200 import _lib, device  # noqa: E402
 
 
 def run_engine(params, parsed, stride: int, n: int, leaf: int, steps: int, warmup: int):
+    """One job per step; under torchrun every rank holds all parsed items, owns its
+    home items (peer tier) and takes leaf chunks from the cross-GPU work queue."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     items = parsed if isinstance(parsed, torch.Tensor) else torch.from_numpy(parsed).cuda()
-    eng = device.DeviceEngine(params, leaf_block=leaf, device_slots=n)
+    multi = world > 1
+    eng = device.DeviceEngine(params, leaf_block=leaf, device_slots=n, rank=rank, world=world,
+                              device=torch.cuda.current_device(), peer_tier=multi, steal=multi)
     total = n * (n - 1) // 2
     out = torch.zeros(total, dtype=torch.float64, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
-    for _ in range(warmup):
+
+    class _At:
+        def __init__(self, off):
+            self.off = off
+
+        def data_ptr(self):
+            return items.data_ptr() + self.off
+
+    connected = [False]
+
+    def step():
+        if multi:
+            eng.load_home(device_items=_At(rank * stride), parsed_stride=world * stride)
+            if not connected[0]:
+                eng.connect_peers()
+                connected[0] = True
+            eng.queue_reset()
+            dist.barrier()
         eng.run(out, device_items=items, parsed_stride=stride)
+        if multi:
+            dist.barrier()
+
+    for _ in range(warmup):
+        step()
     eng.reset_stats()
     torch.cuda.synchronize()
+    if multi:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(estream)
     for _ in range(steps):
-        eng.run(out, device_items=items, parsed_stride=stride)
+        step()
     e1.record(estream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     st = eng.stats()
+    if multi:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([st["pairs_done"], st["steals"], st["peer_fetches"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        st = dict(st, pairs_done=int(c[0].item()) // steps, steals=int(c[1].item()),
+                  peer_fetches=int(c[2].item()))
     eng.close()
     return ms, st, out
 
@@ -67,7 +107,7 @@ def bench_gmm(args):
     pairs = n * (n - 1) // 2
     exps = args.angles * (msum.sum() ** 2 - (msum ** 2).sum()) / 2.0
     clk_ghz = args.clock_ghz
-    sfu_peak = 148 * 16 * clk_ghz * 1e9
+    sfu_peak = 148 * 16 * clk_ghz * 1e9 * int(os.environ.get("WORLD_SIZE", "1"))   # whole box
     return {"app": "gmm", "workload": f"particle fusion, N={n} particles of ~300 localizations, K={args.angles} "
                                       f"rotations (BASELINE configs[3])",
             "pairs": pairs, "ms_per_job": ms, "pairs_per_s": pairs / (ms / 1e3),
@@ -118,12 +158,14 @@ def bench_cv(args):
             hbm = float(json.load(fh).get("hbm_gbs", hbm))
     except Exception:
         pass
+    hbm *= int(os.environ.get("WORLD_SIZE", "1"))   # whole box
     return {"app": "cv", "workload": f"composition-vector cosine, N={n} items, nnz lognormal in [1e5, 1.8e6] "
-                                     f"(mean {nnz.mean():.0f}, max {nnz.max()}) (BASELINE configs[4], 1 GPU)",
+                                     f"(mean {nnz.mean():.0f}, max {nnz.max()}) (BASELINE configs[4])",
             "pairs": pairs, "ms_per_job": ms, "pairs_per_s": pairs / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved_gbs": alg / (ms / 1e3) / 1e9, "peak_gbs": hbm,
                          "frac": alg / (ms / 1e3) / 1e9 / hbm, "alg_bytes_per_job": alg},
-            "launches": st["kernel_launches"]}
+            "launches": st["kernel_launches"], "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steals": st.get("steals"), "peer_fetches": st.get("peer_fetches")}
 
 
 def main():
@@ -138,12 +180,23 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--clock-ghz", type=float, default=1.965)
     args = ap.parse_args()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        lr = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    rank0 = int(os.environ.get("RANK", "0")) == 0
     if args.app == "gmm":
         args.items = args.items or 1000
-        print(json.dumps(bench_gmm(args)), flush=True)
+        line = bench_gmm(args)
     else:
         args.items = args.items or 2500
-        print(json.dumps(bench_cv(args)), flush=True)
+        line = bench_cv(args)
+    if rank0:
+        print(json.dumps(line), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
