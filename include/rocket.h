@@ -222,6 +222,21 @@ rk_status rk_ipc_close(void* d_ptr);
 /* Sample CUDA-event timing of every `every`-th compare batch (0 = off), at most
  * max_samples per run, on the engine's stream. */
 rk_status rk_engine_set_profiling(rk_engine* eng, int every, int max_samples);
+
+/* Trace events of the last run (the reference's metrics.py TraceEvent, one per
+ * compare batch on the gpu lane and per load / peer-fetch group on the up lane),
+ * device timestamps in ns from the start of the run.  max_events = 0 disables. */
+typedef struct {
+  int32_t lane;      /* 0: compare batch, 1: load (H2D + preprocess), 2: peer fetch */
+  int32_t i;         /* first pair's i (compare) or first key loaded */
+  int32_t j;         /* first pair's j, or -1 */
+  int32_t count;     /* pairs in the batch, or items */
+  int64_t start_ns;
+  int64_t end_ns;
+} rk_trace_event;
+rk_status rk_engine_set_trace(rk_engine* eng, int32_t max_events);
+/* Copies up to cap events to out (may be NULL) and returns how many were recorded. */
+int64_t rk_engine_trace_get(const rk_engine* eng, rk_trace_event* out, int64_t cap);
 /* Summed device time, count and pair total of the sampled compare launches of the last run. */
 rk_status rk_engine_kernel_time(const rk_engine* eng, double* ms_total, int64_t* samples, int64_t* pairs);
 /* The engine's cudaStream_t (for callers that order their own work after a run). */

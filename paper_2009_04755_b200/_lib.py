@@ -84,6 +84,11 @@ class EngineStats(C.Structure):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
+class TraceEvent(C.Structure):
+    _fields_ = [("lane", C.c_int32), ("i", C.c_int32), ("j", C.c_int32), ("count", C.c_int32),
+                ("start_ns", C.c_int64), ("end_ns", C.c_int64)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/rocket.h
 SIGNATURES = [
     ("rk_abi_version", C.c_int, []),
@@ -121,6 +126,8 @@ SIGNATURES = [
     ("rk_engine_load_home", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     ("rk_engine_load_home_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32]),
     ("rk_engine_set_peer_homes", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rk_engine_set_trace", C.c_int, [C.c_void_p, C.c_int32]),
+    ("rk_engine_trace_get", C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     ("rk_engine_peer_bandwidth", C.c_int, [C.c_void_p, C.c_int32, C.c_size_t, C.POINTER(C.c_double)]),
     ("rk_engine_queue_word", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("rk_engine_queue_reset", C.c_int, [C.c_void_p]),

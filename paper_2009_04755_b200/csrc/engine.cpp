@@ -255,6 +255,16 @@ struct rk_engine {
   std::vector<const char*> peer_home;   // per rank: base of its home region (own entry = local)
   bool peers_ready = false;
   // sampled kernel timing of the compare batches
+  // trace events (metrics.py TraceEvent): one per compare batch / load group / fetch group
+  struct TraceRec {
+    int32_t lane, i, j, count;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> tr_pool;
+  std::vector<TraceRec> tr;
+  cudaEvent_t tr_t0 = nullptr;
+  int tr_max = 0;
+  std::vector<rk_trace_event> tr_done;
   int profile_every = 0;
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_pairs;
@@ -270,6 +280,25 @@ struct LoadReq {
   int32_t slot;
 };
 
+// Device timestamps of the finished run's trace records, relative to its start.
+rk_status trace_collect(rk_engine* e) {
+  for (const auto& r : e->tr) {
+    float a = 0.f, b = 0.f;
+    RK_CUDA(cudaEventElapsedTime(&a, e->tr_t0, r.a));
+    RK_CUDA(cudaEventElapsedTime(&b, e->tr_t0, r.b));
+    rk_trace_event ev{};
+    ev.lane = r.lane;
+    ev.i = r.i;
+    ev.j = r.j;
+    ev.count = r.count;
+    ev.start_ns = (int64_t)((double)a * 1e6);
+    ev.end_ns = (int64_t)((double)b * 1e6);
+    e->tr_done.push_back(ev);
+  }
+  e->tr.clear();
+  return RK_OK;
+}
+
 // One queue operation on `word` (own or a peer's), synchronous.
 rk_status queue_call(rk_engine* e, unsigned long long* word, int op, unsigned long long arg, unsigned long long* res) {
   queue_op_kernel<<<1, 1, 0, e->cstream>>>(word, op, arg, e->d_qres);
@@ -277,6 +306,18 @@ rk_status queue_call(rk_engine* e, unsigned long long* word, int op, unsigned lo
   RK_CUDA(cudaStreamSynchronize(e->cstream));
   *res = *(volatile unsigned long long*)e->h_qres;
   return RK_OK;
+}
+
+// Trace record around work on `st` (no-op unless rk_engine_set_trace is on)
+int trace_begin(rk_engine* e, int lane, int i, int j, int count, cudaStream_t st) {
+  if (e->tr_max == 0 || (int)e->tr.size() >= e->tr_max) return -1;
+  const size_t k = e->tr.size();
+  e->tr.push_back(rk_engine::TraceRec{lane, i, j, count, e->tr_pool[2 * k], e->tr_pool[2 * k + 1]});
+  cudaEventRecord(e->tr.back().a, st);
+  return (int)k;
+}
+void trace_end(rk_engine* e, int k, cudaStream_t st) {
+  if (k >= 0) cudaEventRecord(e->tr[k].b, st);
 }
 
 rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, uint8_t* d_flags) {
@@ -291,7 +332,9 @@ rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, u
     const bool timed = e->profile_every > 0 && (e->stats.tiles % e->profile_every) == 0 &&
                        e->ev_used + 2 <= (int)e->ev.size();
     if (timed) RK_CUDA(cudaEventRecord(e->ev[e->ev_used], e->stream));
+    const int tk = trace_begin(e, 0, pend[base].i, pend[base].j, m, e->stream);
     RK_TRY(compare_pairs(e->app, e->arena, e->slot_stride, pend.data() + base, m, d_out, d_flags, e->stream));
+    trace_end(e, tk, e->stream);
     if (timed) {
       RK_CUDA(cudaEventRecord(e->ev[e->ev_used + 1], e->stream));
       e->ev_pairs[e->ev_used / 2] = m;
@@ -312,6 +355,7 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
     const int m = (int)std::min<size_t>(e->staging_items, loads.size() - base);
     std::vector<int32_t> slots(m);
     for (int k = 0; k < m; ++k) slots[k] = loads[base + k].slot;
+    const int tk = trace_begin(e, 1, loads[base].key, -1, m, e->lstream);
     if (h_parsed) {
       for (int k = 0; k < m; ++k) {
         const char* src = static_cast<const char*>(h_parsed) + (size_t)loads[base + k].key * parsed_stride;
@@ -331,6 +375,7 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
         k += run;
       }
     }
+    trace_end(e, tk, e->lstream);
     e->stats.loads += m;
   }
   for (const LoadReq& l : loads) e->tier->publish(l.slot, true);  // retained lease (slotcache.py:188-213)
@@ -403,6 +448,8 @@ void rk_engine_destroy(rk_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->tr_pool) cudaEventDestroy(ev);
+  if (e->tr_t0) cudaEventDestroy(e->tr_t0);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->lstream) cudaStreamDestroy(e->lstream);
   if (e->ev_loaded) cudaEventDestroy(e->ev_loaded);
@@ -450,6 +497,9 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->tier->evictions = ev;
   }
   const int64_t launches0 = e->app->launches;
+  e->tr.clear();
+  e->tr_done.clear();
+  if (e->tr_max > 0) RK_CUDA(cudaEventRecord(e->tr_t0, e->stream));
   // the load stream starts after everything already queued on the engine stream
   RK_CUDA(cudaEventRecord(e->ev_compared, e->stream));
   RK_CUDA(cudaStreamWaitEvent(e->lstream, e->ev_compared, 0));
@@ -480,6 +530,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     e->stats.pairs_done += mine;
     e->stats.tiles += 1;
     RK_CUDA(cudaStreamSynchronize(e->stream));
+    RK_TRY(trace_collect(e));
     e->stats.hits = e->tier->hits;
     e->stats.misses = e->tier->misses;
     e->stats.evictions = e->tier->evictions;
@@ -548,6 +599,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     if (!fetches.empty()) {
       // peer tier hit: copy the preprocessed item from its home GPU over NVLink
       const size_t sb = e->app->slot_bytes;
+      const int tk = trace_begin(e, 2, fetches[0].key, -1, (int)fetches.size(), e->lstream);
       for (const LoadReq& f : fetches) {
         const char* src = e->peer_home[f.key % world] + (size_t)(f.key / world) * e->slot_stride;
         char* dst = static_cast<char*>(e->arena) + (size_t)f.slot * e->slot_stride;
@@ -556,6 +608,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
         e->stats.peer_fetches += 1;
         e->stats.peer_bytes += (int64_t)sb;
       }
+      trace_end(e, tk, e->lstream);
       fetches.clear();
       RK_CUDA(cudaEventRecord(e->ev_loaded, e->lstream));
       e->loads_unsynced = true;
@@ -618,6 +671,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   (void)world;
   RK_CUDA(cudaStreamSynchronize(e->lstream));
   RK_CUDA(cudaStreamSynchronize(e->stream));
+  RK_TRY(trace_collect(e));
   e->stats.steals = e->steals;
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;
@@ -638,6 +692,30 @@ rk_status rk_engine_reset_stats(rk_engine* e) {
   e->steals = 0;
   e->tier->hits = e->tier->misses = e->tier->waits = e->tier->evictions = 0;
   return RK_OK;
+}
+
+rk_status rk_engine_set_trace(rk_engine* e, int32_t max_events) {
+  if (!e || max_events < 0) return set_error(RK_ERR_VALUE, "bad trace argument");
+  RK_CUDA(cudaSetDevice(e->device));
+  for (cudaEvent_t ev : e->tr_pool) cudaEventDestroy(ev);
+  e->tr_pool.clear();
+  e->tr.clear();
+  e->tr_done.clear();
+  e->tr_max = max_events;
+  if (max_events > 0) {
+    e->tr_pool.resize((size_t)2 * max_events);
+    for (auto& ev : e->tr_pool) RK_CUDA(cudaEventCreate(&ev));
+    if (!e->tr_t0) RK_CUDA(cudaEventCreate(&e->tr_t0));
+  }
+  return RK_OK;
+}
+
+int64_t rk_engine_trace_get(const rk_engine* e, rk_trace_event* out, int64_t cap) {
+  if (!e) return -1;
+  const int64_t n = (int64_t)e->tr_done.size();
+  if (out)
+    for (int64_t k = 0; k < std::min(n, cap); ++k) out[k] = e->tr_done[(size_t)k];
+  return n;
 }
 
 rk_status rk_engine_kernel_time(const rk_engine* e, double* ms_total, int64_t* samples, int64_t* pairs) {

@@ -135,6 +135,27 @@ class DeviceEngine:
     def set_profiling(self, every: int, max_samples: int = 1024) -> None:
         check(lib.rk_engine_set_profiling(self.handle, every, max_samples))
 
+    _TRACE_LANES = {0: ("gpu", "compare"), 1: ("up", "preprocess"), 2: ("up", "fetch")}
+
+    def set_trace(self, max_events: int) -> None:
+        """Record up to max_events trace events per run (0 disables)."""
+        check(lib.rk_engine_set_trace(self.handle, max_events))
+
+    def trace(self, node: int = 0) -> list[dict]:
+        """The last run's events in the reference's TraceEvent schema (metrics.py:14-29):
+        lane gpu<d> for compare batches, up<d> for loads / peer fetches; i, j = first
+        pair (or first key and -1) of the group; ns from the start of the run."""
+        n = int(lib.rk_engine_trace_get(self.handle, None, 0))
+        buf = (_lib.TraceEvent * max(1, n))()
+        lib.rk_engine_trace_get(self.handle, buf, n)
+        out = []
+        for ev in buf[:n]:
+            kind, label = self._TRACE_LANES[int(ev.lane)]
+            out.append({"node": node, "lane": f"{kind}{self.device}", "label": label,
+                        "start_ns": int(ev.start_ns), "end_ns": int(ev.end_ns), "i": int(ev.i), "j": int(ev.j),
+                        "count": int(ev.count)})
+        return out
+
     def kernel_time(self) -> tuple[float, int, int]:
         """(summed ms, sampled launches, pairs in those launches) of the last run."""
         ms = C.c_double()

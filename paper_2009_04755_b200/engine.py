@@ -40,6 +40,8 @@ class RunResult:
     flags: np.ndarray                  # uint8   [C(n,2)] wire-encoded match
     stats: dict = field(default_factory=dict)
     seconds: float = 0.0
+    trace: list = field(default_factory=list)      # metrics.py TraceEvent dicts (when tracing)
+    node: dict = field(default_factory=dict)       # this rank's NodeMetrics dict
 
     @property
     def pairs(self) -> int:
@@ -104,7 +106,7 @@ class AllPairsEngine:
 
     def __init__(self, app: B200Application, *, leaf_block: int = 16, device_slots: Optional[int] = None,
                  rank: int = 0, world: int = 1, peer_tier: bool = True, steal: bool = True,
-                 steal_chunk: int = 0):
+                 steal_chunk: int = 0, trace_events: int = 0):
         self.app = app
         self.rank = rank
         self.world = world
@@ -115,6 +117,10 @@ class AllPairsEngine:
                                  peer_tier=peer_tier and world > 1 and app.kind not in (0, 3),
                                  steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk)
         self._peers_connected = False
+        self._slots = max(2, slots)
+        if trace_events:
+            self._eng.set_trace(trace_events)
+        self._trace_on = bool(trace_events)
         self._out = torch.empty(app.n * (app.n - 1) // 2, dtype=torch.float64, device=f"cuda:{app.device}")
         self._flags = torch.empty_like(self._out, dtype=torch.uint8)
 
@@ -173,7 +179,27 @@ class AllPairsEngine:
             gather_triangle(self._out, self._flags)
         values = self._out.cpu().numpy()
         flags = self._flags.cpu().numpy()
-        return RunResult(self.app.n, values, flags, self._eng.stats(), time.perf_counter() - t0)
+        seconds = time.perf_counter() - t0
+        stats = self._eng.stats()
+        events = self._eng.trace(node=self.rank) if self._trace_on else []
+        from .metrics import node_metrics
+        return RunResult(self.app.n, values, flags, stats, seconds, events,
+                         node_metrics(self.rank, stats, seconds, self._slots, events))
+
+    def metrics(self, result: RunResult, config: Optional[dict] = None,
+                costs: Optional[perfmodel.StageCosts] = None) -> dict:
+        """RunMetrics document (metrics.py:89-159) of a run, NodeMetrics of every rank."""
+        from .metrics import run_metrics
+        per_node = [result.node]
+        makespan = result.seconds
+        if self.world > 1:
+            import torch.distributed as dist
+            gathered = [None] * self.world
+            dist.all_gather_object(gathered, (result.node, result.seconds))
+            per_node = [g[0] for g in gathered]
+            makespan = max(g[1] for g in gathered)
+        cfg = config if config is not None else {"app": self.app.name, "n": self.app.n, "world": self.world}
+        return run_metrics(cfg, self.app.n, per_node, makespan, costs=costs, wall_time=result.seconds)
 
 
 def run_allpairs(app: B200Application, **kw) -> RunResult:

@@ -183,3 +183,30 @@ def test_engine_2048_with_evictions():
     assert np.array_equal(flags.cpu().numpy() == 3, got >= 60.0)
     st = eng.stats()
     assert st["pairs_done"] == total and st["evictions"] > 0
+
+
+def test_engine_trace_events_and_metrics(tmp_path):
+    """Trace events (reference TraceEvent schema) cover every compare batch and load
+    group; the RunMetrics document reports R, hit rate and the perf-model efficiency."""
+    from paper_2009_04755_b200 import metrics, perfmodel
+    from paper_2009_04755_b200.apps import PCEApp
+    from paper_2009_04755_b200.engine import AllPairsEngine
+    app = PCEApp(20, side=256, cameras=3, seed=4)
+    eng = AllPairsEngine(app, leaf_block=4, device_slots=8, trace_events=4096)
+    res = eng.run()
+    ev = res.trace
+    comp = [e for e in ev if e["label"] == "compare"]
+    loads = [e for e in ev if e["label"] == "preprocess"]
+    assert sum(e["count"] for e in comp) == res.pairs == res.stats["pairs_done"]
+    assert sum(e["count"] for e in loads) == res.stats["loads"]
+    assert all(e["lane"] == "gpu0" for e in comp) and all(e["lane"] == "up0" for e in loads)
+    assert all(0 <= e["start_ns"] <= e["end_ns"] for e in ev)
+    starts = [e["start_ns"] for e in comp]
+    assert starts == sorted(starts)                     # one stream: batches in order
+    path = tmp_path / "trace.jsonl"
+    metrics.write_trace(str(path), ev)
+    assert len(metrics.read_trace(str(path))) == len(ev)
+    doc = eng.metrics(res, costs=perfmodel.StageCosts(t_preprocess=1e-5, t_comparison=1e-5))
+    assert doc["R"] == res.r_factor and doc["pairs"] == res.pairs
+    assert doc["per_node"][0]["comparisons"] == res.pairs and doc["efficiency"] > 0
+    eng.close()
