@@ -210,3 +210,24 @@ def test_engine_trace_events_and_metrics(tmp_path):
     assert doc["R"] == res.r_factor and doc["pairs"] == res.pairs
     assert doc["per_node"][0]["comparisons"] == res.pairs and doc["efficiency"] > 0
     eng.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_engine_tiny_jobs(n):
+    """Degenerate job sizes: n = 1 has no pairs (nothing written, no launch needed),
+    n = 2 and 3 one partial leaf."""
+    _l, device = _lib()
+    side = 256
+    items = make_items(max(n, 1), side, cameras=1, seed=2)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=8)
+    total = n * (n - 1) // 2
+    out = torch.full((max(total, 1),), float("nan"), dtype=torch.float64, device="cuda")
+    eng.run(out, device_items=items, parsed_stride=side * side * 4)
+    st = eng.stats()
+    assert st["pairs_done"] == total
+    got = out.cpu().numpy()
+    if total == 0:
+        assert np.isnan(got[0])
+    else:
+        want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
+        np.testing.assert_allclose(got[:total], want, rtol=RTOL)
