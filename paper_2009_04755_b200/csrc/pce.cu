@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       const int cbeg = q * NCOL + 4 * wg, cend = (q + 1) * NCOL;
       uint64_t* bar = &s_bar[wg][0];
       if (leader) {
-        fence_proxy_async();
+        refill_fence();
         mbar_expect_tx(bar, 2 * kHalfBytes);
         bulk_g2s_hint(gb, Xs + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
         bulk_g2s_hint(gb + kHalf, Ys + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
         }
         named_bar(1 + wg, kGW * 32);   // this group's slices are consumed
         if (leader && c0 + 8 < cend) {
-          fence_proxy_async();
+          refill_fence();
           mbar_expect_tx(bar, 2 * kHalfBytes);
           bulk_g2s_hint(gb, Xs + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
           bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
         block8_rows_z<R>(v, gb + buf * kHalf, gi, lane);
         named_bar(1 + wg, kGW * 32);   // the block is consumed: refill it
         if (leader && rb + 4 < bend) {
-          fence_proxy_async();
+          refill_fence();
           mbar_expect_tx(&s_bar[wg][1 + buf], kHalfBytes);
           bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 4) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
                         pol_first);

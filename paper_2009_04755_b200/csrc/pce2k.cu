@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, c
       auto issue = [&](int u) {
         const int cq = wg + 2 * (u >> 1), p = u & 1;
         const size_t off = ((size_t)p * NC + 4 * cq) * H;
-        fence_proxy_async();
+        fence_proxy_async();   // measured: dropping it here is not faster at 2048^2
         mbar_expect_tx(bar, 2 * kUnitBytes);
         bulk_g2s_hint(gb, Xs + off, kUnitBytes, bar, pol);
         bulk_g2s_hint(gb + kUnitF2, Ys + off, kUnitBytes, bar, pol);

@@ -14,6 +14,18 @@ constexpr int kWin = 11;                // PCE exclusion neighbourhood side
 constexpr int kHalfWin = kWin / 2;
 constexpr int kMeanParts = 64;          // CTAs per item in the mean reduction
 
+// Refilling a staging buffer that was only READ by generic loads (the values are
+// already in registers, ordered by the group barrier) needs no proxy fence: the
+// generic -> async proxy fence is only required after generic WRITES.  ncu put
+// ~8 % of the compare kernel's stall samples on these per-refill fences (they
+// also wait for the leader's outstanding T stores).  -DPCE_REFILL_FENCE=1 restores them.
+#ifndef PCE_REFILL_FENCE
+#define PCE_REFILL_FENCE 0
+#endif
+__device__ __forceinline__ void refill_fence() {
+  if (PCE_REFILL_FENCE) fence_proxy_async();
+}
+
 __device__ __forceinline__ bool better(float v, int idx, float bv, int bidx) {
   return v > bv || (v == bv && idx < bidx);
 }
