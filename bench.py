@@ -55,6 +55,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-steal", action="store_true", help="N > 1: static leaf shares, no cross-GPU stealing")
+    ap.add_argument("--app", default="pce", choices=["pce", "gmm", "cv"],
+                    help="pce: configs[1] (default); gmm: configs[3]; cv: configs[4]")
+    ap.add_argument("--angles", type=int, default=36, help="gmm: rotation grid K")
+    ap.add_argument("--mean-nnz", type=float, default=5e5, help="cv: mean tokens per item")
     return ap.parse_args()
 
 
@@ -176,6 +180,240 @@ def cpu_baseline(n, side, cameras, seed, budget_s):
                       f"({wall:.1f}s wall incl. spawn and generation)"}
 
 
+def _gmm_worker(args):
+    keys, seed, angles, budget = args
+    from oracle import gmm as ogmm
+    from paper_2009_04755_b200.synthdata import particle
+    parts = {k: particle(k, seed) for k in keys}          # load stage, untimed
+    done, t0 = 0, time.perf_counter()
+    for ai, a in enumerate(keys):
+        for b in keys[ai + 1:]:
+            ogmm.compare(parts[a], parts[b], angles)
+            done += 1
+            if time.perf_counter() - t0 > budget:
+                return done, time.perf_counter() - t0
+    return done, time.perf_counter() - t0
+
+
+def _cv_worker(args):
+    sizes, seed, budget = args
+    from oracle import cv as ocv
+    from paper_2009_04755_b200.synthdata import cv_parsed_host
+    blobs = cv_parsed_host(sizes, seed)                    # load stage, untimed
+    done, t0 = 0, time.perf_counter()
+    vecs = {}
+    for a in range(len(blobs)):
+        for b in range(a + 1, len(blobs)):
+            for k in (a, b):
+                if k not in vecs:
+                    vecs[k] = ocv.preprocess(blobs[k])     # count -> freq, charged like the GPU preprocess
+            ocv.compare(vecs[a], vecs[b])
+            done += 1
+            if time.perf_counter() - t0 > budget:
+                return done, time.perf_counter() - t0
+    return done, time.perf_counter() - t0
+
+
+def cpu_baseline_app(app, n, seed, budget_s, angles=36, mean_nnz=5e5):
+    """The oracle's CPU compare (oracle/gmm.py numpy, oracle/cv.py the reference's
+    sequential merge restated) on all host cores over a bounded pair sample."""
+    import multiprocessing as mp
+    import random
+    cores = os.cpu_count() or 1
+    rng = random.Random(seed)
+    if app == "gmm":
+        jobs = []
+        for _ in range(cores):
+            base = rng.randrange(0, max(1, n - 24))
+            jobs.append((list(range(base, min(n, base + 24))), seed, angles, budget_s))
+        worker, what = _gmm_worker, f"particle pairs (K={angles}, numpy float64)"
+    else:
+        from paper_2009_04755_b200.synthdata import cv_nnz
+        sizes = cv_nnz(n, mean_nnz, seed)
+        jobs = [([int(x) for x in sizes[rng.randrange(0, n - 6):][:6]], seed + w, budget_s) for w in range(cores)]
+        worker, what = _cv_worker, "composition-vector pairs (pure-Python merge of the reference's compare)"
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(worker, jobs)
+    wall = time.perf_counter() - t0
+    pairs = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"value": pairs / busy, "unit": "pairs/s", "cores": cores, "kind": "port",
+            "sample": f"{pairs} {what} on {cores} processes, {busy:.1f}s timed ({wall:.1f}s wall incl. "
+                      f"spawn and item generation)"}
+
+
+def main_app(args, rank, world, local_rank):
+    """gmm (configs[3]) / cv (configs[4]): same contract as the PCE line."""
+    import numpy as np
+    n = args.items if args.items != 4096 else (1000 if args.app == "gmm" else 2500)
+    pairs_total = n * (n - 1) // 2
+    if args.app == "gmm":
+        workload = (f"particle fusion (GMM/Bhattacharyya), N={n} particles of ~300 localizations, "
+                    f"K={args.angles} rotations (BASELINE configs[3])")
+    else:
+        workload = (f"composition-vector cosine, N={n} variable-length items, nnz lognormal in [1e5, 1.8e6] "
+                    f"(mean {args.mean_nnz:.0f}) (BASELINE configs[4])")
+    metric = "pairs/sec (whole box)"
+    budget = max(3.0, args.cpu_seconds / 3)
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        vals, cb = [], None
+        for _ in range(max(1, args.warmup) + args.steps):
+            cb = cpu_baseline_app(args.app, n, args.seed, budget, args.angles, args.mean_nnz)
+            vals.append(cb["value"])
+        value = sum(vals[args.warmup:] or vals) / len(vals[args.warmup:] or vals)
+        print(json.dumps({"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": 0,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * pairs_total / value,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": workload, "n": n,
+                                                          "parallelism": f"cpu{cb['cores']}"},
+                          "cpu_baseline": dict(cb, value=value),
+                          "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_2009_04755_b200 import _lib, device
+    from paper_2009_04755_b200.engine import gather_triangle
+    from paper_2009_04755_b200 import synthdata
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    if args.app == "gmm":
+        host_np, msum = synthdata.gmm_parsed(n, args.seed, 400)
+        stride = host_np.shape[1]
+        items = torch.from_numpy(host_np.reshape(-1)).cuda()
+        params = _lib.app_params(_lib.APP_GMM, n, max_entries=400, gmm_angles=args.angles)
+        work = args.angles * (float(msum.sum()) ** 2 - float((msum.astype(np.float64) ** 2).sum())) / 2.0
+    else:
+        items, stride, cap, nnz = synthdata.cv_parsed_device(n, args.mean_nnz, args.seed)
+        params = _lib.app_params(_lib.APP_CV, n, max_entries=cap, threshold=0.5)
+        work = 16.0 * (n - 1) * float(nnz.sum())   # sum over pairs of 16 (nnz_i + nnz_j) bytes
+    multi = world > 1
+    eng = device.DeviceEngine(params, leaf_block=16, device_slots=n, rank=rank, world=world, device=local_rank,
+                              peer_tier=multi, steal=multi and not args.no_steal)
+    out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
+    estream = torch.cuda.ExternalStream(eng.stream())
+
+    class _At:
+        def __init__(self, t, off):
+            self.t, self.off = t, off
+
+        def data_ptr(self):
+            return self.t.data_ptr() + self.off
+
+    state = {"connected": False}
+
+    def step(host=None):
+        src = host if host is not None else items
+        if multi:
+            eng.load_home(**({"host_items": _At(src, rank * stride)} if host is not None
+                             else {"device_items": _At(src, rank * stride)}), parsed_stride=world * stride)
+            if not state["connected"]:
+                eng.connect_peers()
+                state["connected"] = True
+            if eng.steal:
+                eng.queue_reset()
+            barrier()
+        eng.run(out, flags, **({"host_items": host} if host is not None else {"device_items": items}),
+                parsed_stride=stride)
+        if multi:
+            barrier()
+
+    for _ in range(args.warmup):
+        step()
+    eng.reset_stats()
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(estream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(estream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    st = eng.stats()
+    t = torch.tensor([ms, float(st["pairs_done"])], dtype=torch.float64, device="cuda")
+    if multi:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms = float(tmax[0])
+    value = float(t[1]) / (ms / 1e3)
+    e2e = None
+    parsed_total = n * stride
+    if not args.no_e2e and parsed_total <= (24 << 30):
+        host = torch.empty(parsed_total, dtype=torch.uint8, pin_memory=True)
+        host.copy_(items)
+        res_host = torch.empty(pairs_total, dtype=torch.float64, pin_memory=True)
+        step(host)
+        eng.reset_stats()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step(host)
+            gather_triangle(out, flags)
+            res_host.copy_(out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        st2 = eng.stats()
+        if multi:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs_total * args.steps / (float(ems[0]) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(st2["h2d_bytes"] // max(1, args.steps)),
+               "d2h_bytes_per_step": pairs_total * 8}
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    per_job_s = ms / 1e3 / args.steps
+    if args.app == "gmm":
+        peak = 148 * 16 * sm_mhz * 1e6 * world
+        roofline = {"bound": "sfu", "achieved": work / per_job_s / 1e12, "peak": peak / 1e12, "unit": "Tex2/s",
+                    "frac": work / per_job_s / peak, "traffic": None,
+                    "peak_source": f"148 SMs x 16 MUFU.EX2/clk x measured {sm_mhz:.0f} MHz x {world} GPU(s)",
+                    "kernel": "gmm_pair_kernel (CTA per pair x 12-angle block)", "ex2_per_job": work}
+    else:
+        peaks, src = load_peaks()
+        peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])) * world
+        roofline = {"bound": "hbm", "achieved": work / per_job_s / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": work / per_job_s / 1e9 / peak, "traffic": None, "peak_source": src,
+                    "kernel": "cv_work (merge-path units, coalesced token windows)",
+                    "alg_bytes_per_job": work}
+    cpu = None
+    if rank == 0 and not args.no_cpu and world == 1:
+        cpu = cpu_baseline_app(args.app, n, args.seed, budget, args.angles, args.mean_nnz)
+    if rank == 0:
+        print(json.dumps({"metric": metric, "value": value, "unit": "pairs/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "fp32" if args.app == "gmm" else "fp64", "data": "synthetic",
+                          "config": {"workload": workload, "n": n, "pairs": pairs_total, "leaf_block": 16,
+                                     "parallelism": f"pairs{world}",
+                                     "l2": f"items {parsed_total / 2**30:.1f} GiB parsed"},
+                          "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+                          "gpu_launches": st["kernel_launches"],
+                          "cache": {"R": st["loads"] / n, "device_hit_rate":
+                                    st["hits"] / max(1, st["hits"] + st["misses"]),
+                                    "steals": st["steals"], "peer_fetches": st["peer_fetches"]}}), flush=True)
+    eng.close()
+    if multi:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------------------
 
 def main():
@@ -183,6 +421,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.app != "pce":
+        return main_app(args, rank, world, local_rank)
     n, side = args.items, args.side
     pairs_total = n * (n - 1) // 2
     cfg_name = {(4096, 1024): " (BASELINE configs[1])", (16384, 2048): " (BASELINE configs[2])"}.get((n, side), "")

@@ -92,16 +92,10 @@ def run_engine(params, parsed, stride: int, n: int, leaf: int, steps: int, warmu
 
 
 def bench_gmm(args):
-    from paper_2009_04755_b200.synthdata import particle
+    from paper_2009_04755_b200.synthdata import gmm_parsed
     n, maxp = args.items, 400
     stride = 8 + 12 * maxp
-    host = np.zeros((n, stride), dtype=np.uint8)
-    msum = np.zeros(n)
-    for k in range(n):
-        p = particle(k, args.seed)
-        msum[k] = len(p)
-        host[k, :8] = np.frombuffer(np.array([len(p), 0], dtype="<u4").tobytes(), dtype=np.uint8)
-        host[k, 8:8 + 12 * len(p)] = np.frombuffer(p.astype("<f4").tobytes(), dtype=np.uint8)
+    host, msum = gmm_parsed(n, args.seed, maxp)
     params = _lib.app_params(_lib.APP_GMM, n, max_entries=maxp, gmm_angles=args.angles)
     ms, st, _ = run_engine(params, host.reshape(-1), stride, n, args.leaf, args.steps, args.warmup)
     pairs = n * (n - 1) // 2
@@ -117,32 +111,9 @@ def bench_gmm(args):
             "launches": st["kernel_launches"]}
 
 
-def cv_items(n: int, mean_nnz: float, seed: int, vocab_bits: int = 26):
-    """Sparse composition vectors in the reference's parsed format, skewed nnz,
-    generated on the device (torch) straight into the parsed buffer."""
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    rng = np.random.default_rng(seed)
-    nnz = np.clip(rng.lognormal(np.log(mean_nnz), 0.6, size=n), 1e5, 1.8e6).astype(np.int64)
-    cap = int(nnz.max())
-    stride = (4 + 12 * cap + 15) // 16 * 16
-    buf = torch.zeros(n * stride, dtype=torch.uint8, device="cuda")
-    pools = {}
-    for k in range(n):
-        fam = k % 16
-        if fam not in pools:   # a family's shared token pool -> non-trivial cosines
-            pools[fam] = torch.randint(0, 1 << vocab_bits, (2_000_000,), generator=g, device="cuda")
-        m = int(nnz[k])
-        shared = pools[fam][torch.randint(0, 2_000_000, (m // 2,), generator=g, device="cuda")]
-        own = torch.randint(0, 1 << vocab_bits, (m - m // 2,), generator=g, device="cuda")
-        tok = torch.unique(torch.cat([shared, own]))          # sorted, unique
-        cnt = torch.randint(1, 50, (tok.numel(),), generator=g, device="cuda", dtype=torch.int32)
-        rec = torch.cat([tok.view(torch.uint8).view(-1, 8), cnt.view(torch.uint8).view(-1, 4)], dim=1).reshape(-1)
-        base = k * stride
-        buf[base:base + 4] = torch.tensor([tok.numel()], dtype=torch.int32, device="cuda").view(torch.uint8)
-        buf[base + 4:base + 4 + rec.numel()] = rec
-        nnz[k] = tok.numel()
-    torch.cuda.synchronize()
-    return buf, stride, cap, nnz
+def cv_items(n: int, mean_nnz: float, seed: int):
+    from paper_2009_04755_b200.synthdata import cv_parsed_device
+    return cv_parsed_device(n, mean_nnz, seed)
 
 
 def bench_cv(args):
