@@ -86,6 +86,9 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
+        if os.environ.get("RK_NO_CLOCKS"):   # diagnosis: measure without the sampler
+            self.proc = None
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
