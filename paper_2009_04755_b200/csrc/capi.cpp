@@ -27,6 +27,23 @@ rk_status check_cuda(cudaError_t err, const char* what) {
   return set_error(RK_ERR_DEVICE, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
 }
 
+rk_status status_begin(rk_app* app, cudaStream_t s, int** d_status) {
+  if (!app->d_status) {
+    RK_CUDA(cudaMalloc(&app->d_status, sizeof(int)));
+    RK_CUDA(cudaHostAlloc(&app->h_status, sizeof(int), cudaHostAllocDefault));
+  }
+  RK_CUDA(cudaMemsetAsync(app->d_status, 0, sizeof(int), s));
+  *d_status = app->d_status;
+  return RK_OK;
+}
+
+rk_status status_end(rk_app* app, cudaStream_t s, int* h_status) {
+  RK_CUDA(cudaMemcpyAsync(app->h_status, app->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  *h_status = *app->h_status;
+  return RK_OK;
+}
+
 size_t stride_pad(const char* env, size_t dflt) {
   const char* v = getenv(env);
   if (!v || !*v) return dflt;
@@ -170,6 +187,8 @@ void rk_app_destroy(rk_app* app) {
   if (app->p.kind == RK_APP_NCC) ncc_free(app);
   delete app->job;
   cudaFree(app->gmm_scratch);
+  cudaFree(app->d_status);
+  if (app->h_status) cudaFreeHost(app->h_status);
   cudaFree(app->cv_scratch);
   delete app;
 }

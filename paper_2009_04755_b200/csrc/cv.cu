@@ -270,8 +270,7 @@ rk_status cv_init(rk_app* app) {
 rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                         size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s) {
   int* d_status = nullptr;
-  RK_CUDA(cudaMallocAsync(&d_status, sizeof(int), s));
-  RK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  RK_TRY(status_begin(app, s, &d_status));
   for (int base = 0; base < n_items; base += kMaxBatch) {
     const int m = n_items - base < kMaxBatch ? n_items - base : kMaxBatch;
     SlotList dst;
@@ -284,9 +283,7 @@ rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
     RK_CUDA(cudaGetLastError());
   }
   int h_status = 0;
-  RK_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  RK_CUDA(cudaFreeAsync(d_status, s));
-  RK_CUDA(cudaStreamSynchronize(s));
+  RK_TRY(status_end(app, s, &h_status));
   if (h_status == RK_ERR_SLOT_OVERFLOW)
     return set_error(RK_ERR_SLOT_OVERFLOW, "preprocessed item exceeds slot capacity of %d entries", app->p.max_entries);
   if (h_status == RK_ERR_MALFORMED) return set_error(RK_ERR_MALFORMED, "parsed item has no k-mers");

@@ -72,6 +72,29 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x for x <= 0 on the FMA pipe (no MUFU): round-to-nearest split x = j + f via
+// the 1.5 * 2^23 magic constant, degree-5 polynomial for 2^f on [-0.5, 0.5]
+// (relative error 7.7e-8), exponent added as an integer.  Arguments below -125
+// return ~0 (the Gauss terms there are < 1e-37 of the peak).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;
+  const int j = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(0.0013266970386325856f, f, 0.00967545974551767f);
+  p = fmaf(p, f, 0.0555074261600255f);
+  p = fmaf(p, f, 0.24022121753561645f);
+  p = fmaf(p, f, 0.6931469491610631f);
+  p = fmaf(p, f, 1.0000000710296983f);
+  return __int_as_float(__float_as_int(p) + (j << 23));
+}
+
+// angles of a block whose exponentials go to the FMA pipe instead of the SFU,
+// balancing the two pipes (the kernel is SFU-bound otherwise)
+#ifndef GMM_POLY
+#define GMM_POLY 2
+#endif
+
 // grid = pairs x angle blocks: CTA (p, ab) evaluates angles 12ab .. 12ab+11 of
 // pair p and stores its best E_k in blk_best[p * nblk + ab]; gmm_finalize takes
 // the max over the blocks (order-independent: deterministic).  Splitting the
@@ -132,7 +155,8 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PceJob 
 #pragma unroll
           for (int t = 0; t < kAngBlock; ++t) {
             const float dot = fmaf(rx[t], q.x, ry[t] * q.y);
-            acc[t] += ex2_approx(fmaf(dot, w2, base));
+            const float arg = fmaf(dot, w2, base);
+            acc[t] += (t < GMM_POLY) ? ex2_poly(arg) : ex2_approx(arg);
           }
         }
       }
@@ -190,8 +214,7 @@ rk_status gmm_init(rk_app* app) {
 rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                          size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s) {
   int* d_status = nullptr;
-  RK_CUDA(cudaMallocAsync(&d_status, sizeof(int), s));
-  RK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  RK_TRY(status_begin(app, s, &d_status));
   for (int base = 0; base < n_items; base += kMaxBatch) {
     const int m = n_items - base < kMaxBatch ? n_items - base : kMaxBatch;
     SlotList dst;
@@ -204,9 +227,7 @@ rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
     RK_CUDA(cudaGetLastError());
   }
   int h_status = 0;
-  RK_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  RK_CUDA(cudaFreeAsync(d_status, s));
-  RK_CUDA(cudaStreamSynchronize(s));
+  RK_TRY(status_end(app, s, &h_status));
   if (h_status == RK_ERR_SLOT_OVERFLOW)
     return set_error(RK_ERR_SLOT_OVERFLOW, "particle exceeds %d localizations", app->p.max_entries);
   if (h_status == RK_ERR_MALFORMED) return set_error(RK_ERR_MALFORMED, "particle has no localizations");

@@ -90,6 +90,8 @@ struct rk_app {
   int32_t slot_group = 1;  // slots interleaved in groups of this many (rk_app_slot_group)
   rk::PceJob* job = nullptr;   // host staging of by-value pair lists (GMM, CV launches)
   double* gmm_scratch = nullptr;   // per (pair, angle block) best of one GMM launch
+  int* d_status = nullptr;          // preprocess status word (device) and its pinned host mirror
+  int* h_status = nullptr;
   void* cv_scratch = nullptr;       // CV unit offsets, work counter and unit partials
   int cv_grid = 0;                  // persistent CV work grid (SMs x resident CTAs)
   rk::PceState pce;
@@ -136,6 +138,11 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
                    double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 double threshold_or_nan(const rk_app* app);
+// Preprocess status word: reset on `s` (allocated once per app; no per-call
+// cudaMallocAsync, whose pool trimming stalled the load stream for ~0.5 s), then
+// read back after the kernels (synchronous on `s`).
+rk_status status_begin(rk_app* app, cudaStream_t s, int** d_status);
+rk_status status_end(rk_app* app, cudaStream_t s, int* h_status);
 // Padding (bytes) added to power-of-two per-item / per-CTA strides (env RK_SLOT_PAD / RK_T_PAD)
 size_t stride_pad(const char* env, size_t dflt);
 

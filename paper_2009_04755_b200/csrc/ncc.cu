@@ -508,8 +508,7 @@ rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
     return set_error(RK_ERR_VALUE, "NCC strides must be multiples of 16 bytes");
   const int64_t d = (int64_t)app->p.height * app->p.width;
   int* d_status = nullptr;
-  RK_CUDA(cudaMallocAsync(&d_status, sizeof(int), s));
-  RK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), s));
+  RK_TRY(status_begin(app, s, &d_status));
   const size_t stride_f = parsed_stride / sizeof(float);
   constexpr int kParts = 64;
   for (int base = 0; base < n_items; base += kMaxBatch) {
@@ -525,9 +524,7 @@ rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
     RK_CUDA(cudaGetLastError());
   }
   int h_status = 0;
-  RK_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
-  RK_CUDA(cudaFreeAsync(d_status, s));
-  RK_CUDA(cudaStreamSynchronize(s));
+  RK_TRY(status_end(app, s, &h_status));
   if (h_status == RK_ERR_MALFORMED) return set_error(RK_ERR_MALFORMED, "NCC item has zero variance");
   return RK_OK;
 }
