@@ -190,6 +190,7 @@ void rk_app_destroy(rk_app* app) {
   cudaFree(app->d_status);
   if (app->h_status) cudaFreeHost(app->h_status);
   cudaFree(app->cv_scratch);
+  cudaFree(app->cv_prep);
   delete app;
 }
 

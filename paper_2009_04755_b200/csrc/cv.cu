@@ -20,57 +20,78 @@ namespace rk {
 
 namespace {
 
-__device__ __forceinline__ uint32_t ld_u32_unaligned(const uint8_t* p) {
-  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+// Preprocess, three kernels per batch of items (grid = kPrepParts chunks x items,
+// so a load group keeps the whole GPU busy):
+//   cvp_sum    integer sum of the counts (exact, order-free atomics)
+//   cvp_write  tokens and freq = count / total into the slot, per-chunk sum of freq^2
+//   cvp_final  fixed-order sum of the chunks -> norm, slot header, status
+// The parsed records (<Q token><I count>, 12 B) are 4-byte aligned: three u32 loads.
+constexpr int kPrepParts = 32;
+
+__device__ __forceinline__ bool cv_item_ok(uint32_t dim, int cap) { return dim != 0 && (int64_t)dim <= cap; }
+
+__global__ void __launch_bounds__(256) cvp_sum(const uint8_t* __restrict__ parsed, size_t parsed_stride, int cap,
+                                               unsigned long long* __restrict__ totals) {
+  const int item = blockIdx.y;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(parsed + (size_t)item * parsed_stride);
+  const uint32_t dim = src[0];
+  if (!cv_item_ok(dim, cap)) return;
+  unsigned long long t = 0;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < dim; k += gridDim.x * blockDim.x)
+    t += __ldg(src + 1 + 3 * (size_t)k + 2);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0 && t) atomicAdd(&totals[item], t);
 }
 
-__device__ __forceinline__ uint64_t ld_u64_unaligned(const uint8_t* p) {
-  return (uint64_t)ld_u32_unaligned(p) | ((uint64_t)ld_u32_unaligned(p + 4) << 32);
-}
-
-// One CTA per item.
-__global__ void cv_preprocess_kernel(const uint8_t* __restrict__ parsed, size_t parsed_stride, SlotList dst,
-                                     uint8_t* __restrict__ slots, size_t slot_stride, int cap,
-                                     int* __restrict__ status) {
-  const int item = blockIdx.x;
-  const uint8_t* src = parsed + (size_t)item * parsed_stride;
-  const uint32_t dim = ld_u32_unaligned(src);
+__global__ void __launch_bounds__(256) cvp_write(const uint8_t* __restrict__ parsed, size_t parsed_stride,
+                                                 SlotList dst, uint8_t* __restrict__ slots, size_t slot_stride, int cap,
+                                                 const unsigned long long* __restrict__ totals,
+                                                 double* __restrict__ part) {
+  const int item = blockIdx.y;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(parsed + (size_t)item * parsed_stride);
+  const uint32_t dim = src[0];
+  if (!cv_item_ok(dim, cap)) return;
+  const double total = (double)totals[item];
   uint8_t* slot = slots + (size_t)dst.idx[item] * slot_stride;
-  if (dim == 0 || (int64_t)dim > cap) {
-    if (threadIdx.x == 0) atomicMax(status, dim == 0 ? (int)RK_ERR_MALFORMED : (int)RK_ERR_SLOT_OVERFLOW);
-    return;
-  }
-  __shared__ unsigned long long s_total;
-  __shared__ double s_sq;
-  if (threadIdx.x == 0) {
-    s_total = 0ull;
-    s_sq = 0.0;
-  }
-  __syncthreads();
-  unsigned long long tot = 0;
-  for (uint32_t k = threadIdx.x; k < dim; k += blockDim.x) tot += ld_u32_unaligned(src + 4 + 12 * (size_t)k + 8);
-  atomicAdd(&s_total, tot);
-  __syncthreads();
-  const double total = (double)s_total;
   uint64_t* tok = reinterpret_cast<uint64_t*>(slot + 16);
   double* freq = reinterpret_cast<double*>(slot + 16 + 8 * (size_t)cap);
   double sq = 0.0;
-  for (uint32_t k = threadIdx.x; k < dim; k += blockDim.x) {
-    const uint8_t* e = src + 4 + 12 * (size_t)k;
-    const double f = (double)ld_u32_unaligned(e + 8) / total;
-    tok[k] = ld_u64_unaligned(e);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < dim; k += gridDim.x * blockDim.x) {
+    const uint32_t* e = src + 1 + 3 * (size_t)k;
+    const double f = (double)__ldg(e + 2) / total;
+    tok[k] = (uint64_t)__ldg(e) | ((uint64_t)__ldg(e + 1) << 32);
     freq[k] = f;
     sq = fma(f, f, sq);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_sq, sq);
+  __shared__ double s_sq[8];
+  if ((threadIdx.x & 31) == 0) s_sq[threadIdx.x >> 5] = sq;
   __syncthreads();
   if (threadIdx.x == 0) {
-    *reinterpret_cast<uint32_t*>(slot) = dim;
-    *reinterpret_cast<uint32_t*>(slot + 4) = 0u;
-    *reinterpret_cast<double*>(slot + 8) = sqrt(s_sq);
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sq[w];
+    part[(size_t)item * gridDim.x + blockIdx.x] = t;
   }
+}
+
+__global__ void cvp_final(const uint8_t* __restrict__ parsed, size_t parsed_stride, int n_items, SlotList dst,
+                          uint8_t* __restrict__ slots, size_t slot_stride, int cap, const double* __restrict__ part,
+                          int* __restrict__ status) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= n_items) return;
+  const uint32_t dim = *reinterpret_cast<const uint32_t*>(parsed + (size_t)item * parsed_stride);
+  if (!cv_item_ok(dim, cap)) {
+    atomicMax(status, dim == 0 ? (int)RK_ERR_MALFORMED : (int)RK_ERR_SLOT_OVERFLOW);
+    return;
+  }
+  double sq = 0.0;
+  for (int c = 0; c < kPrepParts; ++c) sq += part[(size_t)item * kPrepParts + c];
+  uint8_t* slot = slots + (size_t)dst.idx[item] * slot_stride;
+  *reinterpret_cast<uint32_t*>(slot) = dim;
+  *reinterpret_cast<uint32_t*>(slot + 4) = 0u;
+  *reinterpret_cast<double*>(slot + 8) = sqrt(sq);
 }
 
 // Merge-path split: number of A elements among the first `diag` merged
@@ -269,17 +290,30 @@ rk_status cv_init(rk_app* app) {
 
 rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride, int n_items, void* d_slots,
                         size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s) {
+  if (parsed_stride % 4 != 0) return set_error(RK_ERR_VALUE, "CV parsed_stride must be a multiple of 4 bytes");
+  if (!app->cv_prep) {   // totals [kMaxBatch] u64 | partials [kMaxBatch * kPrepParts] f64
+    RK_CUDA(cudaMalloc(&app->cv_prep, sizeof(unsigned long long) * kMaxBatch +
+                                          sizeof(double) * kMaxBatch * kPrepParts));
+  }
+  unsigned long long* totals = static_cast<unsigned long long*>(app->cv_prep);
+  double* part = reinterpret_cast<double*>(totals + kMaxBatch);
   int* d_status = nullptr;
   RK_TRY(status_begin(app, s, &d_status));
+  const uint8_t* parsed = static_cast<const uint8_t*>(d_parsed);
+  uint8_t* slots = static_cast<uint8_t*>(d_slots);
   for (int base = 0; base < n_items; base += kMaxBatch) {
     const int m = n_items - base < kMaxBatch ? n_items - base : kMaxBatch;
     SlotList dst;
     dst.n = m;
     for (int k = 0; k < m; ++k) dst.idx[k] = h_slot_idx[base + k];
-    cv_preprocess_kernel<<<m, 256, 0, s>>>(static_cast<const uint8_t*>(d_parsed) + (size_t)base * parsed_stride,
-                                           parsed_stride, dst, static_cast<uint8_t*>(d_slots), slot_stride,
-                                           app->p.max_entries, d_status);
-    app->launches += 1;
+    const uint8_t* px = parsed + (size_t)base * parsed_stride;
+    RK_CUDA(cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * m, s));
+    cvp_sum<<<dim3(kPrepParts, m), 256, 0, s>>>(px, parsed_stride, app->p.max_entries, totals);
+    cvp_write<<<dim3(kPrepParts, m), 256, 0, s>>>(px, parsed_stride, dst, slots, slot_stride, app->p.max_entries,
+                                                   totals, part);
+    cvp_final<<<(m + 63) / 64, 64, 0, s>>>(px, parsed_stride, m, dst, slots, slot_stride, app->p.max_entries, part,
+                                           d_status);
+    app->launches += 3;
     RK_CUDA(cudaGetLastError());
   }
   int h_status = 0;

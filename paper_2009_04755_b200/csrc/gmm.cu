@@ -92,7 +92,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // angles of a block whose exponentials go to the FMA pipe instead of the SFU,
 // balancing the two pipes (the kernel is SFU-bound otherwise)
 #ifndef GMM_POLY
-#define GMM_POLY 2
+#define GMM_POLY 0   // measured: 0 (all MUFU) 478 ms, 2: 489 ms, 3: 500 ms per C4 job
 #endif
 
 // grid = pairs x angle blocks: CTA (p, ab) evaluates angles 12ab .. 12ab+11 of

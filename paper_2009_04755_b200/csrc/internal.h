@@ -93,6 +93,7 @@ struct rk_app {
   int* d_status = nullptr;          // preprocess status word (device) and its pinned host mirror
   int* h_status = nullptr;
   void* cv_scratch = nullptr;       // CV unit offsets, work counter and unit partials
+  void* cv_prep = nullptr;          // CV preprocess totals and norm partials
   int cv_grid = 0;                  // persistent CV work grid (SMs x resident CTAs)
   rk::PceState pce;
   rk::NccState ncc;
