@@ -18,7 +18,7 @@ from paper_2009_04755_b200 import _lib, device, synthdata  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("app", choices=["gmm", "cv"])
+    ap.add_argument("app", choices=["gmm", "cv", "pce"])
     ap.add_argument("--items", type=int, default=0)
     ap.add_argument("--runs", type=int, default=4)
     a = ap.parse_args()
@@ -28,11 +28,17 @@ def main():
         stride = host.shape[1]
         items = torch.from_numpy(host.reshape(-1)).cuda()
         params = _lib.app_params(_lib.APP_GMM, n, max_entries=400, gmm_angles=36)
+    elif a.app == "pce":
+        n, side = a.items or 1024, 1024
+        items = torch.empty(n * side * side, dtype=torch.float32, device="cuda")
+        device.synth_prnu(side, side, 0, n, 64, 1, items)
+        stride = side * side * 4
+        params = _lib.app_params(_lib.APP_PCE, n, height=side, width=side, threshold=60.0)
     else:
         n = a.items or 600
         items, stride, cap, _ = synthdata.cv_parsed_device(n, 5e5, 1)
         params = _lib.app_params(_lib.APP_CV, n, max_entries=cap)
-    eng = device.DeviceEngine(params, leaf_block=16, device_slots=n)
+    eng = device.DeviceEngine(params, leaf_block=8 if a.app == "pce" else 16, device_slots=n)
     eng.set_trace(100000)
     out = torch.zeros(n * (n - 1) // 2, dtype=torch.float64, device="cuda")
     for r in range(a.runs):
