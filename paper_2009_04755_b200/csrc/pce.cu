@@ -51,6 +51,18 @@ constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] til
 // warps per compare CTA: 8 lane groups (one per row pair of a 16-row block); one CTA per SM
 __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
 
+// Transpose buffer of the compare kernel: XOR-swizzled R*R (default) or padded
+// R*(R+1) for R = 32 (no per-element address registers; -DPCE_PAD_XPOSE=1).
+#ifndef PCE_PAD_XPOSE
+#define PCE_PAD_XPOSE 0
+#endif
+__host__ __device__ constexpr int xpose_size(int R) { return (PCE_PAD_XPOSE && R == 32) ? R * (R + 1) : R * R; }
+template <int R>
+__device__ __forceinline__ void compare_fft(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
+  if constexpr (PCE_PAD_XPOSE && R == 32) group_fft_pad_rt<R, true>(v, xbuf, w, lane);
+  else group_fft_rt<R, true>(v, xbuf, w, lane);
+}
+
 template <int R>
 struct ClusterShape;
 #ifndef PCE_CL
@@ -238,7 +250,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   const bool leader = (tid % (kGW * 32)) == 0;
   const int q = (int)cluster_ctarank();
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  float2* xbuf = xbufs + grp * R * R;
+  float2* xbuf = xbufs + grp * xpose_size(R);
   float2* gb = gbufs + wg * 2 * kHalf;    // this warp group's 2 x 4N float2
   float2* Tp = T + (size_t)cid * t_stride;
   for (int i = tid; i < R * R; i += NT) tw[i] = tw_g[i];
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
           bulk_g2s_hint(gb, Xs + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
           bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
         }
-        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        compare_fft<R>(v, xbuf, twr, lane);
         // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
         const int rr = lane & 7;
         const int pos = (((rr >> 1) ^ ((col >> 1) & 3)) << 1) | (rr & 1);
@@ -372,7 +384,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
           bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 4) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
                         pol_first);
         }
-        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        compare_fft<R>(v, xbuf, twr, lane);
         argmax_update<R>(v, 8 * rb + 2 * gi, lane, m, idx, ss);
       }
     }
@@ -446,7 +458,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
 #pragma unroll
           for (int n2 = 0; n2 < R; ++n2) v[n2] = make_float2(0.f, 0.f);
         }
-        group_fft_rt<R, true>(v, xbuf, twr, lane);
+        compare_fft<R>(v, xbuf, twr, lane);
         const bool va = ((ra - rstart + N) & (N - 1)) < kWin;
         const bool vb = ((ra + 1 - rstart + N) & (N - 1)) < kWin;
         float w = 0.f;
@@ -490,7 +502,7 @@ template <int R>
 size_t cluster_smem() {
   constexpr int N = R * R;
   // 2 warp groups x 2 x 4N (column slices / 8-row blocks) + twiddles + one transpose per lane group
-  return (size_t)(16 * N + R * R + cta_warps(R) * (32 / R) * R * R) * sizeof(float2);
+  return (size_t)(16 * N + R * R + cta_warps(R) * (32 / R) * xpose_size(R)) * sizeof(float2);
 }
 
 template <int R>
