@@ -77,3 +77,33 @@ def test_two_ranks_peer_fetch_match_oracle(steal_chunk, delay0):
     if delay0 > 0:
         assert outs[1][3]["steals"] >= 1                         # the idle rank stole from the late one
         assert outs[1][3]["pairs_done"] > outs[0][3]["pairs_done"]
+
+
+def test_three_ranks_steal_from_a_late_rank():
+    """Three ranks (IPC-shared cuda:0): rank 0 starts 3 s late, the other two drain
+    their shares and then steal from it -- and from each other's stolen ranges --
+    while every pair is still computed exactly once and matches the oracle."""
+    import torch.multiprocessing as mp
+    from oracle import pce as opce
+    from paper_2009_04755_b200.apps import PCEApp
+    world = 3
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, ret, 1, 3.0)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([ret.get(timeout=300) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    values = sum(o[1] for o in outs)
+    flags = sum(o[2].astype(np.int32) for o in outs)
+    app = PCEApp(26, side=256, cameras=3, seed=17)
+    pats = np.stack([np.frombuffer(app.fetch_raw(app.path_for_key(k)), dtype=np.float32).reshape(256, 256)
+                     for k in range(26)])
+    np.testing.assert_allclose(values, opce.all_pairs(pats), rtol=1e-4)
+    assert set(np.unique(flags)) <= {1, 3}
+    assert sum(o[3]["pairs_done"] for o in outs) == 26 * 25 // 2
+    assert outs[1][3]["steals"] + outs[2][3]["steals"] >= 1
+    assert outs[0][3]["pairs_done"] < min(outs[1][3]["pairs_done"], outs[2][3]["pairs_done"])
