@@ -169,6 +169,8 @@ typedef struct {
   int64_t peer_fetches;    /* items copied from a peer GPU's home region (the remote tier, distcache.py) */
   int64_t peer_bytes;
   int64_t steals;          /* chunks this rank stole from other ranks' queues */
+  int64_t pinned_at_end;   /* device slots still leased when the run returned (must be 0) */
+  int64_t writing_at_end;  /* device slots still in WRITE when the run returned (must be 0) */
 } rk_engine_stats;
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,

@@ -78,6 +78,8 @@ class EngineStats(C.Structure):
         ("peer_fetches", C.c_int64),
         ("peer_bytes", C.c_int64),
         ("steals", C.c_int64),
+        ("pinned_at_end", C.c_int64),
+        ("writing_at_end", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -673,6 +673,13 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   RK_CUDA(cudaStreamSynchronize(e->stream));
   RK_TRY(trace_collect(e));
   e->stats.steals = e->steals;
+  // lease hygiene at run end (test_engine.py:124-133): no reader, no slot in WRITE
+  e->stats.pinned_at_end = 0;
+  e->stats.writing_at_end = 0;
+  for (int q = 0; q < e->tier->capacity; ++q) {
+    e->stats.pinned_at_end += e->tier->readers[q] > 0;
+    e->stats.writing_at_end += e->tier->state[q] == kWrite;
+  }
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;
   e->stats.evictions = e->tier->evictions;

@@ -141,6 +141,7 @@ def test_engine_matches_oracle(device_slots, leaf):
     want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=RTOL)
     assert st["pairs_done"] == total
+    assert st["pinned_at_end"] == 0 and st["writing_at_end"] == 0     # lease hygiene (test_engine.py:124-133)
     if device_slots >= n:
         assert st["loads"] == n and st["evictions"] == 0   # R = 1 at capacity >= n
     else:
