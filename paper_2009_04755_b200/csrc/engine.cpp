@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "internal.h"
@@ -552,7 +553,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   std::vector<int32_t> pinned;
   std::vector<int32_t> slot_of(peer ? n : 0, -1);
   const int lim = batch_limit(e->app);
-  auto do_leaf = [&](const Leaf& l) -> rk_status {
+  std::function<rk_status(const Leaf&)> do_leaf = [&](const Leaf& l) -> rk_status {
     if (e->app->p.kind == RK_APP_SYNTHETIC) {
       // no item state: the hash needs only the keys (apps.py:201-208)
       RK_TRY(rk_compare_tile(e->app, nullptr, 0, l.r0, l.r1, l.c0, l.c1, nullptr, d_out, d_flags, e->stream));
@@ -566,6 +567,21 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
     for (int32_t k = l.c0; k < l.c1; ++k) keys.push_back(k);
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    {
+      // tight tier (test_engine.py:88-93 "tight tier completes"): a leaf whose items do
+      // not fit the device slots is split into its quadrants (Region.split,
+      // scheduler.py:56-68) until they do; a 1 x 1 region needs 2 slots
+      int64_t need = 0;
+      for (int32_t k : keys) need += !(peer && k % world == e->p.rank);
+      if (need > e->tier->capacity && (l.r1 - l.r0 > 1 || l.c1 - l.c0 > 1)) {
+        const int32_t rm = (l.r0 + l.r1 + 1) / 2, cm = (l.c0 + l.c1 + 1) / 2;
+        const Leaf q[4] = {{l.r0, rm, l.c0, cm}, {l.r0, rm, cm, l.c1}, {rm, l.r1, l.c0, cm}, {rm, l.r1, cm, l.c1}};
+        for (const Leaf& sub : q)
+          if (sub.r0 < sub.r1 && sub.c0 < sub.c1 && region_pairs(sub.r0, sub.r1, sub.c0, sub.c1) > 0)
+            RK_TRY(do_leaf(sub));
+        return RK_OK;
+      }
+    }
     pinned.clear();
     for (int32_t k : keys) {
       if (peer && k % world == e->p.rank) {

@@ -232,3 +232,20 @@ def test_engine_tiny_jobs(n):
     else:
         want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
         np.testing.assert_allclose(got[:total], want, rtol=RTOL)
+
+
+def test_engine_tight_tier_completes():
+    """Two device slots with 8-item leaves: leaves are split until their items fit
+    (the reference's tight-tier completion, test_engine.py:88-93); results exact."""
+    _l, device = _lib()
+    side, n = 256, 9
+    items = make_items(n, side, cameras=2, seed=13)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=8,
+                              device_slots=2)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    eng.run(out, device_items=items, parsed_stride=side * side * 4)
+    want = opce.all_pairs(items.cpu().numpy().reshape(n, side, side))
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=RTOL)
+    st = eng.stats()
+    assert st["pairs_done"] == total and st["pinned_at_end"] == 0 and st["evictions"] > 0
