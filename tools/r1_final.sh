@@ -1,0 +1,5 @@
+# final round-1 evidence on one GPU: bench line, launch list, full ncu of one pce_cluster launch
+set -x
+timeout 900 python bench.py > gpurun_out/final_bench.log 2>&1; echo BENCH $? >> gpurun_out/final_bench.log
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/final_ncu_list.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:pce_cluster -s 6 -c 1 -o gpurun_out/prof_final python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/final_ncu_full.log 2>&1
