@@ -153,7 +153,7 @@ __device__ __forceinline__ int cv_units_of(int na, int nb) {
 }
 
 // one CTA of 1024 threads: unit offsets (exclusive scan), total, counter reset
-__global__ void __launch_bounds__(1024) cv_units(const PceJob job, const uint8_t* __restrict__ slots,
+__global__ void __launch_bounds__(1024) cv_units(const PairJob job, const uint8_t* __restrict__ slots,
                                                  size_t slot_stride, int* __restrict__ offsets,
                                                  int* __restrict__ ctl) {
   __shared__ int s_scan[1024];
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(1024) cv_units(const PceJob job, const uint8_t
   }
 }
 
-__global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PceJob job, const uint8_t* __restrict__ slots,
+__global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PairJob job, const uint8_t* __restrict__ slots,
                                                          size_t slot_stride, int cap, const int* __restrict__ offsets,
                                                          int* __restrict__ ctl, double* __restrict__ partial) {
   __shared__ int s_off[1025];
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PceJob job, const
   }
 }
 
-__global__ void cv_finalize(const PceJob job, const uint8_t* __restrict__ slots, size_t slot_stride,
+__global__ void cv_finalize(const PairJob job, const uint8_t* __restrict__ slots, size_t slot_stride,
                             const int* __restrict__ offsets, const double* __restrict__ partial,
                             double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -326,7 +326,7 @@ rk_status cv_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride,
 
 rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                          double* d_out, uint8_t* d_flags, cudaStream_t s) {
-  if (!app->job) app->job = new PceJob();
+  if (!app->job) app->job = new PairJob();
   if (!app->cv_scratch) {
     // offsets [1025] | ctl [2] | partials [1024 * kMaxUnits]
     RK_CUDA(cudaMalloc(&app->cv_scratch, sizeof(int) * 1028 + sizeof(double) * kPipeMaxPairs * kMaxUnits));
@@ -340,7 +340,7 @@ rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, 
   int* ctl = offsets + 1025;
   double* partial = reinterpret_cast<double*>(static_cast<char*>(app->cv_scratch) + sizeof(int) * 1028);
   const uint8_t* slots = static_cast<const uint8_t*>(d_slots);
-  PceJob& job = *app->job;
+  PairJob& job = *app->job;
   for (int base = 0; base < n; base += kPipeMaxPairs) {
     const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
     job.npairs = m;

@@ -99,7 +99,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // pair p and stores its best E_k in blk_best[p * nblk + ab]; gmm_finalize takes
 // the max over the blocks (order-independent: deterministic).  Splitting the
 // angle grid over CTAs gives ~7 waves per 1,024-pair launch instead of 2.3.
-__global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PceJob job, const uint8_t* __restrict__ slots,
+__global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob job, const uint8_t* __restrict__ slots,
                                                                    size_t slot_stride, int angles, float s0,
                                                                    double* __restrict__ blk_best) {
   extern __shared__ float4 Q[];                       // particle j (m_j entries)
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PceJob 
   }
 }
 
-__global__ void gmm_finalize(const PceJob job, int nblk, const double* __restrict__ blk_best,
+__global__ void gmm_finalize(const PairJob job, int nblk, const double* __restrict__ blk_best,
                              double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= job.npairs) return;
@@ -205,7 +205,7 @@ rk_status gmm_init(rk_app* app) {
   const size_t smem = (size_t)cap * sizeof(float4);
   if (smem > 200 * 1024) return set_error(RK_ERR_UNSUPPORTED, "GMM max_entries %d too large for shared memory", cap);
   RK_CUDA(cudaFuncSetAttribute(gmm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (!app->job) app->job = new PceJob();
+  if (!app->job) app->job = new PairJob();
   const int nblk = (app->p.gmm_angles + kAngBlock - 1) / kAngBlock;
   RK_CUDA(cudaMalloc(&app->gmm_scratch, sizeof(double) * kPipeMaxPairs * nblk));
   return RK_OK;
@@ -237,7 +237,7 @@ rk_status gmm_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
 rk_status gmm_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                           double* d_out, uint8_t* d_flags, cudaStream_t s) {
   const size_t smem = (size_t)app->p.max_entries * sizeof(float4);
-  PceJob& job = *app->job;
+  PairJob& job = *app->job;
   for (int base = 0; base < n; base += kPipeMaxPairs) {
     const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
     job.npairs = m;

@@ -48,15 +48,17 @@ struct SlotList {
   int32_t idx[kMaxBatch];
 };
 
+// Pair lists of up to 1,024 pairs (PCE, GMM, CV launches), also passed by value
+// (16 KiB of kernel parameters): slot indices and the packed-triangle pair id.
 constexpr int kPipeMaxPairs = 1024;
 struct DevPair {
   int32_t slot_a;
   int32_t slot_b;
   int64_t pid;
 };
-struct PceJob {
+struct PairJob {
   int32_t npairs;
-  int32_t depth;
+  int32_t depth;   // unused (kept for layout stability)
   DevPair pairs[kPipeMaxPairs];
 };
 struct PceState {
@@ -69,7 +71,7 @@ struct PceState {
   int clusters = 0;        // co-resident compare clusters (= pairs in flight)
   float2* T = nullptr;     // clusters * t_stride: column-pass output, one slot per cluster
   size_t t_stride = 0;     // float2 between T slots: (N/2)*N + padding (breaks the power-of-two stride)
-  PceJob* job = nullptr;   // host staging of the launch parameters
+  PairJob* job = nullptr;   // host staging of the launch parameters
 };
 
 struct CvState {};
@@ -88,7 +90,7 @@ struct rk_app {
   size_t parsed_bytes = 0;
   int64_t launches = 0;    // kernels launched through this app (for bench accounting)
   int32_t slot_group = 1;  // slots interleaved in groups of this many (rk_app_slot_group)
-  rk::PceJob* job = nullptr;   // host staging of by-value pair lists (GMM, CV launches)
+  rk::PairJob* job = nullptr;   // host staging of by-value pair lists (GMM, CV launches)
   double* gmm_scratch = nullptr;   // per (pair, angle block) best of one GMM launch
   int* d_status = nullptr;          // preprocess status word (device) and its pinned host mirror
   int* h_status = nullptr;

@@ -211,7 +211,7 @@ __device__ unsigned long long g_pce_probe[148 * 2 * 8];
 
 template <int R, int CL>
 __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
-    const PceJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
+    const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
@@ -555,7 +555,7 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
                        uint8_t* d_flags, cudaStream_t s) {
   constexpr int CL = ClusterShape<R>::CL;
   PceState& st = app->pce;
-  PceJob& job = *st.job;
+  PairJob& job = *st.job;
   job.npairs = n;
   job.depth = 0;
   for (int k = 0; k < n; ++k) {
@@ -585,7 +585,7 @@ rk_status cluster_init(rk_app* app) {
   st.clusters = clusters;
   st.t_stride = (size_t)(N / 2) * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * clusters));
-  st.job = new PceJob();
+  st.job = new PairJob();
   return RK_OK;
 }
 

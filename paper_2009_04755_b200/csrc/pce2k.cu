@@ -256,7 +256,7 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
   return warp_sum(w);
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PceJob job, const char* __restrict__ slots,
+__global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, const char* __restrict__ slots,
                                                             size_t slot_stride, float2* __restrict__ T, size_t t_stride,
                                                             const float2* __restrict__ tw_g, double* __restrict__ out,
                                                             uint8_t* __restrict__ flags, double threshold) {
@@ -502,7 +502,7 @@ rk_status pce2k_init(rk_app* app) {
   st.clusters = per_sm * sms;
   st.t_stride = (size_t)NC * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * st.clusters));
-  st.job = new PceJob();
+  st.job = new PairJob();
   return RK_OK;
 }
 
@@ -527,7 +527,7 @@ rk_status pce2k_preprocess(rk_app* app, const float* pix, size_t stride_f, int n
 rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, const rk_pair* pairs, int n,
                         double* d_out, uint8_t* d_flags, cudaStream_t s) {
   PceState& st = app->pce;
-  PceJob& job = *st.job;
+  PairJob& job = *st.job;
   job.npairs = n;
   job.depth = 0;
   for (int k = 0; k < n; ++k) {
