@@ -74,7 +74,8 @@ static rk_status check_pairs(const rk_app* app, const rk_pair* h_pairs, int n_pa
 
 int batch_limit(const rk_app* app) {
   // by-value pair lists of up to 1,024 pairs (PairJob) for the heavy apps
-  if (app->p.kind == RK_APP_PCE || app->p.kind == RK_APP_GMM || app->p.kind == RK_APP_CV) return kPipeMaxPairs;
+  if (app->p.kind == RK_APP_PCE) return pce_batch_limit(app);
+  if (app->p.kind == RK_APP_GMM || app->p.kind == RK_APP_CV) return kListPairs;
   return kMaxBatch;
 }
 

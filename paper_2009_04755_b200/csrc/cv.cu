@@ -329,7 +329,7 @@ rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, 
   if (!app->job) app->job = new PairJob();
   if (!app->cv_scratch) {
     // offsets [1025] | ctl [2] | partials [1024 * kMaxUnits]
-    RK_CUDA(cudaMalloc(&app->cv_scratch, sizeof(int) * 1028 + sizeof(double) * kPipeMaxPairs * kMaxUnits));
+    RK_CUDA(cudaMalloc(&app->cv_scratch, sizeof(int) * 1028 + sizeof(double) * kListPairs * kMaxUnits));
     int dev = 0, sms = 0, per_sm = 0;
     RK_CUDA(cudaGetDevice(&dev));
     RK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -341,8 +341,8 @@ rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, 
   double* partial = reinterpret_cast<double*>(static_cast<char*>(app->cv_scratch) + sizeof(int) * 1028);
   const uint8_t* slots = static_cast<const uint8_t*>(d_slots);
   PairJob& job = *app->job;
-  for (int base = 0; base < n; base += kPipeMaxPairs) {
-    const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
+  for (int base = 0; base < n; base += kListPairs) {
+    const int m = n - base < kListPairs ? n - base : kListPairs;
     job.npairs = m;
     for (int k = 0; k < m; ++k) {
       const rk_pair& q = pairs[base + k];

@@ -207,7 +207,7 @@ rk_status gmm_init(rk_app* app) {
   RK_CUDA(cudaFuncSetAttribute(gmm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!app->job) app->job = new PairJob();
   const int nblk = (app->p.gmm_angles + kAngBlock - 1) / kAngBlock;
-  RK_CUDA(cudaMalloc(&app->gmm_scratch, sizeof(double) * kPipeMaxPairs * nblk));
+  RK_CUDA(cudaMalloc(&app->gmm_scratch, sizeof(double) * kListPairs * nblk));
   return RK_OK;
 }
 
@@ -238,8 +238,8 @@ rk_status gmm_compare_list(rk_app* app, const void* d_slots, size_t slot_stride,
                           double* d_out, uint8_t* d_flags, cudaStream_t s) {
   const size_t smem = (size_t)app->p.max_entries * sizeof(float4);
   PairJob& job = *app->job;
-  for (int base = 0; base < n; base += kPipeMaxPairs) {
-    const int m = n - base < kPipeMaxPairs ? n - base : kPipeMaxPairs;
+  for (int base = 0; base < n; base += kListPairs) {
+    const int m = n - base < kListPairs ? n - base : kListPairs;
     job.npairs = m;
     for (int k = 0; k < m; ++k) {
       const rk_pair& q = pairs[base + k];

@@ -50,7 +50,9 @@ struct SlotList {
 
 // Pair lists of up to 1,024 pairs (PCE, GMM, CV launches), also passed by value
 // (16 KiB of kernel parameters): slot indices and the packed-triangle pair id.
-constexpr int kPipeMaxPairs = 1024;
+constexpr int kPipeMaxPairs = 1924;   // 13 x 148: whole rounds of the persistent PCE grid
+constexpr int kListPairs = 1024;      // GMM / CV launches (their scans assume <= 1024 pairs)
+int pce_batch_limit(const rk_app* app);
 struct DevPair {
   int32_t slot_a;
   int32_t slot_b;

@@ -591,6 +591,14 @@ rk_status cluster_init(rk_app* app) {
 
 }  // namespace
 
+// Pairs per compare launch: whole rounds of the persistent grid (one pair per CTA
+// per round), so no CTA idles in a launch's last round.
+int pce_batch_limit(const rk_app* app) {
+  const int g = app->pce.clusters > 0 ? app->pce.clusters : 1;
+  const int rounds = kPipeMaxPairs / g;
+  return rounds > 0 ? rounds * g : kPipeMaxPairs;
+}
+
 void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, float* mean_part, cudaStream_t s) {
   pce_mean_partial<<<dim3(kMeanParts, n_items), 256, 0, s>>>(pix, stride_f, nn, mean_part);
 }
@@ -598,8 +606,9 @@ void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, flo
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s) {
   const char* slots = static_cast<const char*>(d_slots);
-  for (int base = 0; base < n; base += kPipeMaxPairs) {
-    const int m = std::min(kPipeMaxPairs, n - base);
+  const int lim = pce_batch_limit(app);
+  for (int base = 0; base < n; base += lim) {
+    const int m = std::min(lim, n - base);
     if (app->pce.N == 2048) RK_TRY(pce2k_compare(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
     else if (app->pce.R == 16) RK_TRY(compare_impl<16>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
     else RK_TRY(compare_impl<32>(app, slots, slot_stride, pairs + base, m, d_out, d_flags, s));
