@@ -242,6 +242,7 @@ struct rk_engine {
   unsigned long long* d_qres = nullptr;
   cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
   int64_t steals = 0;
+  bool queue_armed = false;         // rk_engine_queue_reset since the last run
   void* arena = nullptr;
   size_t slot_stride = 0;
   size_t arena_slots = 0;           // device_slots rounded up to the app's slot group
@@ -542,6 +543,9 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   const bool steal = e->p.steal && e->p.world > 1;
   if (steal && !e->queues_ready)
     return set_error(RK_ERR_VALUE, "work stealing: call rk_engine_queue_reset and rk_engine_set_peer_queues first");
+  if (steal && !e->queue_armed)
+    return set_error(RK_ERR_VALUE, "work stealing: rk_engine_queue_reset (and a barrier) must precede every run");
+  e->queue_armed = false;
   const bool peer = e->home_slots > 0;
   if (peer && !e->peers_ready)
     return set_error(RK_ERR_VALUE, "peer tier: call rk_engine_load_home and rk_engine_set_peer_homes first");
@@ -859,7 +863,9 @@ rk_status rk_engine_queue_reset(rk_engine* e) {
   RK_CUDA(cudaSetDevice(e->device));
   const auto rr = rank_range(quadtree_leaves(e->app->p.n, e->p.leaf_block), e->p.rank, e->p.world);
   unsigned long long tmp = 0;
-  return queue_call(e, e->qword, 3, ((unsigned long long)rr.first << 32) | (unsigned)rr.second, &tmp);
+  RK_TRY(queue_call(e, e->qword, 3, ((unsigned long long)rr.first << 32) | (unsigned)rr.second, &tmp));
+  e->queue_armed = true;
+  return RK_OK;
 }
 
 rk_status rk_engine_set_peer_queues(rk_engine* e, int32_t world, void* const* d_words) {
