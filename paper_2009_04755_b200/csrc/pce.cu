@@ -49,7 +49,12 @@ constexpr int kGroups = 8;              // FFT groups (row-pairs / columns) per 
 constexpr int kRows = 2 * kGroups;      // rows per preprocess row-pass CTA
 constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] tile
 // warps per compare CTA: 8 lane groups (one per row pair of a 16-row block); one CTA per SM
-__host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
+// Warp groups (4 lane groups each) per compare CTA: 2 (default: one CTA of 8 warps
+// per SM) or 1 (-DPCE_GROUPS=1: two independent 4-warp CTAs per SM, each on its own pair).
+#ifndef PCE_GROUPS
+#define PCE_GROUPS 2
+#endif
+__host__ __device__ constexpr int cta_warps(int R) { return 4 * PCE_GROUPS / (32 / R); }
 
 // Transpose buffer of the compare kernel: XOR-swizzled R*R (default) or padded
 // R*(R+1) for R = 32 (no per-element address registers; -DPCE_PAD_XPOSE=1).
@@ -210,14 +215,15 @@ __device__ unsigned long long g_pce_probe[148 * 2 * 8];
 #endif
 
 template <int R, int CL>
-__global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
+__global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster(
     const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
   constexpr int kCtaWarps = cta_warps(R);
   constexpr int NT = kCtaWarps * 32;
-  constexpr int kGW = kCtaWarps / 2;      // warps per warp group (two independent groups)
+  constexpr int kNG = PCE_GROUPS;         // independent warp groups
+  constexpr int kGW = kCtaWarps / kNG;    // warps per warp group
   constexpr int kGL = kGW * G;            // lane groups per warp group: 4 columns / 4 row pairs per round
   constexpr int NCOL = (N / 2) / CL;      // columns per CTA
   constexpr int NB8 = (N / 8) / CL;       // 8-row blocks per CTA
@@ -227,10 +233,10 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   static_assert(kGL == 4, "a warp group owns 4 lane groups");
   static_assert(NCOL * CL == N / 2 && NCOL % 8 == 0 && NB8 * CL == N / 8 && NB8 % 2 == 0, "cluster split");
   extern __shared__ __align__(128) float2 smem[];
-  float2* gbufs = smem;                   // 2 groups x 2 halves of 4N float2 (column slices / row blocks)
-  float2* tw = smem + 4 * kHalf;          // R*R twiddles
+  float2* gbufs = smem;                   // kNG groups x 2 halves of 4N float2 (column slices / row blocks)
+  float2* tw = smem + 2 * kNG * kHalf;    // R*R twiddles
   float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
-  __shared__ __align__(8) uint64_t s_bar[2][3];   // per group: column slices, row block 0 / 1
+  __shared__ __align__(8) uint64_t s_bar[kNG][3];   // per group: column slices, row block 0 / 1
   __shared__ __align__(8) uint64_t s_wbar;
   __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
   __shared__ float s_wpart[8];            // window energy per row pair, gathered in CTA 0
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   float2* Tp = T + (size_t)cid * t_stride;
   for (int i = tid; i < R * R; i += NT) tw[i] = tw_g[i];
   if (tid == 0) {
-    for (int w = 0; w < 2; ++w)
+    for (int w = 0; w < kNG; ++w)
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
     mbar_init(&s_wbar, 1);
   }
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
         bulk_g2s_hint(gb + kHalf, Ys + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
       }
 #pragma unroll 1
-      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      for (int c0 = cbeg; c0 < cend; c0 += 4 * kNG) {
         const int col = c0 + gi;
         mbar_wait(bar, ph & 1u);
         ph ^= 1u;
@@ -335,11 +341,11 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
           }
         }
         named_bar(1 + wg, kGW * 32);   // this group's slices are consumed
-        if (leader && c0 + 8 < cend) {
+        if (leader && c0 + 4 * kNG < cend) {
           refill_fence();
           mbar_expect_tx(bar, 2 * kHalfBytes);
-          bulk_g2s_hint(gb, Xs + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
-          bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 8) * N, kHalfBytes, bar, pol_spec);
+          bulk_g2s_hint(gb, Xs + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
+          bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
         }
         compare_fft<R>(v, xbuf, twr, lane);
         // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
@@ -364,24 +370,24 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       const int bbeg = q * NB8 + wg, bend = (q + 1) * NB8;
       if (leader) {
         fence_proxy_async();     // T's generic-proxy stores (ordered by the cluster barrier) -> async proxy
-        for (int b = 0; b < 2 && bbeg + 2 * b < bend; ++b) {
+        for (int b = 0; b < 2 && bbeg + kNG * b < bend; ++b) {
           mbar_expect_tx(&s_bar[wg][1 + b], kHalfBytes);
-          bulk_g2s_hint(gb + b * kHalf, Tp + (size_t)(bbeg + 2 * b) * kHalf, kHalfBytes, &s_bar[wg][1 + b],
+          bulk_g2s_hint(gb + b * kHalf, Tp + (size_t)(bbeg + kNG * b) * kHalf, kHalfBytes, &s_bar[wg][1 + b],
                         pol_first);
         }
       }
       int it = 0;
 #pragma unroll 1
-      for (int rb = bbeg; rb < bend; rb += 2, ++it) {
+      for (int rb = bbeg; rb < bend; rb += kNG, ++it) {
         const int buf = it & 1;
         mbar_wait(&s_bar[wg][1 + buf], (ph >> (1 + buf)) & 1u);
         ph ^= 2u << buf;
         block8_rows_z<R>(v, gb + buf * kHalf, gi, lane);
         named_bar(1 + wg, kGW * 32);   // the block is consumed: refill it
-        if (leader && rb + 4 < bend) {
+        if (leader && rb + 2 * kNG < bend) {
           refill_fence();
           mbar_expect_tx(&s_bar[wg][1 + buf], kHalfBytes);
-          bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 4) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
+          bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 2 * kNG) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
                         pol_first);
         }
         compare_fft<R>(v, xbuf, twr, lane);
@@ -434,44 +440,46 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       const int rstart = (prow - kHalfWin + N) & (N - 1);
       const int e0 = rstart & ~1;                              // first aligned row of the 12-row span
       const int b0 = e0 >> 3;
-      const int t = q + CL * warp;                             // row pair t = 0..5 of the span
-      const bool mine = (t < kPairsOfRows);
-      // blocks b0, b0+1, b0+2 (mod N/8) -> buffer slots 0..2 (each 4N float2)
-      bool any = false;
-      for (int w = 0; w < kCtaWarps; ++w) any |= (q + CL * w) < kPairsOfRows;
-      if (any) {
+      const int nblk = ((e0 + 2 * kPairsOfRows - 1) >> 3) - b0 + 1;   // 2 or 3 blocks
+      constexpr int kStage = 2 * kNG;                          // staged blocks per pass (group buffers)
+#pragma unroll 1
+      for (int p0 = 0; p0 < nblk; p0 += kStage) {
+        const int cnt = min(kStage, nblk - p0);
         if (tid == 0) {
           fence_proxy_async();
-          mbar_expect_tx(&s_wbar, 3 * kHalfBytes);
-          for (int j = 0; j < 3; ++j)
-            bulk_g2s_hint(gbufs + j * kHalf, Tp + (size_t)((b0 + j) & (N / 8 - 1)) * kHalf, kHalfBytes, &s_wbar,
-                          pol_first);
+          mbar_expect_tx(&s_wbar, cnt * kHalfBytes);
+          for (int j = 0; j < cnt; ++j)
+            bulk_g2s_hint(gbufs + j * kHalf, Tp + (size_t)((b0 + p0 + j) & (N / 8 - 1)) * kHalf, kHalfBytes,
+                          &s_wbar, pol_first);
         }
         mbar_wait(&s_wbar, wph & 1u);
         wph ^= 1u;
-      }
-      if (mine) {
-        const int ra = (e0 + 2 * t) & (N - 1);                // even row: pair (ra, ra + 1)
-        const int j = ((ra >> 3) - b0 + (N / 8)) & (N / 8 - 1);   // which staged block
-        block8_rows_z<R>(v, gbufs + j * kHalf, (ra & 7) >> 1, lane);
-        if (g != 0) {   // R = 16: the warp's second lane group has no row pair
+#pragma unroll 1
+        for (int t = q + CL * warp; t < kPairsOfRows; t += CL * kCtaWarps) {   // row pair t of the span
+          const int ra = (e0 + 2 * t) & (N - 1);                // even row: pair (ra, ra + 1)
+          const int j = (((ra >> 3) - b0 + (N / 8)) & (N / 8 - 1)) - p0;   // staged slot of its block
+          if (j < 0 || j >= cnt) continue;
+          block8_rows_z<R>(v, gbufs + j * kHalf, (ra & 7) >> 1, lane);
+          if (g != 0) {   // R = 16: the warp's second lane group has no row pair
 #pragma unroll
-          for (int n2 = 0; n2 < R; ++n2) v[n2] = make_float2(0.f, 0.f);
-        }
-        compare_fft<R>(v, xbuf, twr, lane);
-        const bool va = ((ra - rstart + N) & (N - 1)) < kWin;
-        const bool vb = ((ra + 1 - rstart + N) & (N - 1)) < kWin;
-        float w = 0.f;
-#pragma unroll
-        for (int k2 = 0; k2 < R; ++k2) {
-          const int s = lane + R * k2;
-          if (((s - pcol + kHalfWin + N) & (N - 1)) < kWin) {
-            if (va) w = fmaf(v[k2].x, v[k2].x, w);
-            if (vb) w = fmaf(v[k2].y, v[k2].y, w);
+            for (int n2 = 0; n2 < R; ++n2) v[n2] = make_float2(0.f, 0.f);
           }
+          compare_fft<R>(v, xbuf, twr, lane);
+          const bool va = ((ra - rstart + N) & (N - 1)) < kWin;
+          const bool vb = ((ra + 1 - rstart + N) & (N - 1)) < kWin;
+          float w = 0.f;
+#pragma unroll
+          for (int k2 = 0; k2 < R; ++k2) {
+            const int s = lane + R * k2;
+            if (((s - pcol + kHalfWin + N) & (N - 1)) < kWin) {
+              if (va) w = fmaf(v[k2].x, v[k2].x, w);
+              if (vb) w = fmaf(v[k2].y, v[k2].y, w);
+            }
+          }
+          w = warp_sum(w);
+          if (wl == 0) dsmem_st_f32(wpart0 + t * sizeof(float), w);   // fixed-order sum in CTA 0
         }
-        w = warp_sum(w);
-        if (wl == 0) dsmem_st_f32(wpart0 + t * sizeof(float), w);   // fixed-order sum in CTA 0
+        if (p0 + kStage < nblk) cluster_sync();   // staged blocks consumed before the next pass
       }
     }
     PCE_PROBE(5);
@@ -502,7 +510,7 @@ template <int R>
 size_t cluster_smem() {
   constexpr int N = R * R;
   // 2 warp groups x 2 x 4N (column slices / 8-row blocks) + twiddles + one transpose per lane group
-  return (size_t)(16 * N + R * R + cta_warps(R) * (32 / R) * xpose_size(R)) * sizeof(float2);
+  return (size_t)(8 * PCE_GROUPS * N + R * R + cta_warps(R) * (32 / R) * xpose_size(R)) * sizeof(float2);
 }
 
 template <int R>
