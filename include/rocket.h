@@ -133,6 +133,14 @@ rk_status rk_compare_tile(rk_app* app, const void* d_slots, size_t slot_stride,
 rk_status rk_ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t rank,
                       int32_t world, double* d_out, uint8_t* d_flags, void* stream);
 
+/* One block of the NCC Gram over an arena that holds only some items (C3-sized
+ * jobs): A = slots a_row0 .. a_row0+a_cnt-1 holding keys a_key0 .., B likewise;
+ * the same block twice computes its upper triangle, distinct blocks (disjoint
+ * key ranges) all their pairs.  Rows start on slot groups (multiples of 128). */
+rk_status rk_ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                            int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt,
+                            double* d_out, uint8_t* d_flags, void* stream);
+
 /* Deterministic synthetic inputs (test/bench data generators, not the hot path). */
 /* PRNU-like patterns: item k = 0.2*K[k % cameras] + N(0,1), fp32, h*w each. */
 rk_status rk_synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras,
@@ -217,6 +225,12 @@ rk_status rk_engine_peer_bandwidth(rk_engine* eng, int32_t src_rank, size_t byte
 rk_status rk_engine_queue_word(const rk_engine* eng, void** d_word);
 rk_status rk_engine_queue_reset(rk_engine* eng);
 rk_status rk_engine_set_peer_queues(rk_engine* eng, int32_t world, void* const* d_words);
+
+/* Plain device buffers for arenas shared over CUDA IPC (the handle of a cudaMalloc
+ * base pointer) and a stream-ordered device-to-device (or peer, over NVLink) copy. */
+rk_status rk_device_alloc(size_t bytes, int device, void** d_ptr);
+rk_status rk_device_free(void* d_ptr);
+rk_status rk_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 
 rk_status rk_ipc_handle(const void* d_ptr, uint8_t* out_handle64);
 rk_status rk_ipc_open(const uint8_t* handle64, int device, void** d_ptr);

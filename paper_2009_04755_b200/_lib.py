@@ -111,6 +111,8 @@ SIGNATURES = [
                                   C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_void_p]),
     ("rk_ncc_gram", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,
                               C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("rk_ncc_gram_block", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("rk_synth_prnu", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
     ("rk_engine_create", C.c_int, [C.POINTER(AppParams), C.POINTER(EngineParams), C.c_int,
@@ -134,6 +136,9 @@ SIGNATURES = [
     ("rk_engine_queue_word", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("rk_engine_queue_reset", C.c_int, [C.c_void_p]),
     ("rk_engine_set_peer_queues", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("rk_device_alloc", C.c_int, [C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]),
+    ("rk_device_free", C.c_int, [C.c_void_p]),
+    ("rk_memcpy_d2d", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     ("rk_ipc_handle", C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     ("rk_ipc_open", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)]),
     ("rk_ipc_close", C.c_int, [C.c_void_p]),

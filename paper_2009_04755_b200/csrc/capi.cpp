@@ -247,6 +247,33 @@ rk_status rk_ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int3
   return ncc_gram(app, d_slots, slot_stride, n_rows, rank, world, d_out, d_flags, static_cast<cudaStream_t>(stream));
 }
 
+rk_status rk_device_alloc(size_t bytes, int device, void** d_ptr) {
+  if (!d_ptr) return set_error(RK_ERR_VALUE, "null argument");
+  RK_CUDA(cudaSetDevice(device));
+  RK_CUDA(cudaMalloc(d_ptr, bytes));
+  return RK_OK;
+}
+
+rk_status rk_device_free(void* d_ptr) {
+  RK_CUDA(cudaFree(d_ptr));
+  return RK_OK;
+}
+
+rk_status rk_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  RK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return RK_OK;
+}
+
+rk_status rk_ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                            int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt,
+                            double* d_out, uint8_t* d_flags, void* stream) {
+  if (!app || !d_slots || !d_out) return set_error(RK_ERR_VALUE, "null argument");
+  if (app->p.kind != RK_APP_NCC) return set_error(RK_ERR_VALUE, "rk_ncc_gram_block needs an NCC app");
+  RK_CUDA(cudaSetDevice(app->device));
+  return ncc_gram_block(app, d_slots, slot_stride, n_rows, a_row0, a_key0, a_cnt, b_row0, b_key0, b_cnt, d_out,
+                        d_flags, static_cast<cudaStream_t>(stream));
+}
+
 rk_status rk_synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras, uint64_t seed,
                         float* d_out, void* stream) {
   if (h <= 0 || w <= 0 || n_items < 0 || cameras <= 0) return set_error(RK_ERR_VALUE, "bad synth_prnu arguments");

@@ -121,6 +121,9 @@ void pce_launch_mean(const float* pix, size_t stride_f, int nn, int n_items, flo
 
 // NCC Gram tile side for n items (256: CTA-pair kernel, 128: single-CTA kernel)
 int ncc_gram_tile(int n);
+rk_status ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                         int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt, double* d_out,
+                         uint8_t* d_flags, cudaStream_t s);
 
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s);

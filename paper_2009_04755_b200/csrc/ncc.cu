@@ -338,15 +338,27 @@ constexpr int kTile2 = 256;   // items per CTA-pair tile side
 #endif
 constexpr int kChunkBlocks = NCC_KCHUNK;   // k-blocks (x 32 floats) per launch: 64K floats
 
-// One CTA pair (cluster of 2) per upper-triangle 256x256 tile of items.
+// A Gram block: rows of A = slots a_row0 .. a_row0 + a_cnt - 1 holding items (keys)
+// a_key0 .., the same for B; tri = A and B are the same block (upper-triangle
+// tiles only).  Tiles t with t % world == rank are computed.  Slot rows must be
+// multiples of 128 (the interleaved slot groups).  The all-resident Gram is the
+// block (0, 0, n) x (0, 0, n).
+struct GramBlock {
+  int a_row0, a_key0, a_cnt;
+  int b_row0, b_key0, b_cnt;
+  int tri, rank, world;
+  int na, nb;   // 256-item tiles along A and B
+};
+
+// One CTA pair (cluster of 2) per 256x256 tile of a Gram block.
 // K is processed in chunks [kb0, kb1) of k-blocks, one launch each: every CTA of
 // a launch streams the same K window, so the tiles sharing an operand row block
 // read it while it is still in L2 (with K = 1M in one launch the CTAs drift
 // apart and most operand reads miss L2).  Chunk 0 stores, later chunks add
 // (fp64, fixed launch order: deterministic); the last chunk writes the flags.
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid_constant__ CUtensorMap tmap, int n,
-                                                                    int64_t d, int64_t kc, int kb0, int kb1, int tiles_per_side, int rank,
-                                                                    int world, double* __restrict__ out,
+                                                                    int64_t d, int64_t kc, int kb0, int kb1,
+                                                                    const GramBlock blk, double* __restrict__ out,
                                                                     uint8_t* __restrict__ flags, double threshold) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -356,14 +368,20 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
 
-  int t = (blockIdx.x >> 1) * world + rank;
-  int ti = 0;
-  while (t >= tiles_per_side - ti) {
-    t -= tiles_per_side - ti;
-    ++ti;
+  int t = (blockIdx.x >> 1) * blk.world + blk.rank;
+  int ti = 0, tj = 0;
+  if (blk.tri) {
+    while (t >= blk.na - ti) {
+      t -= blk.na - ti;
+      ++ti;
+    }
+    tj = ti + t;
+  } else {
+    ti = t / blk.nb;
+    tj = t % blk.nb;
   }
-  const int tj = ti + t;
-  const int row0 = ti * kTile2 + (int)cta * kTile, col0 = tj * kTile2;
+  const int lrow0 = ti * kTile2 + (int)cta * kTile, lcol0 = tj * kTile2;   // within the block
+  const int row0 = blk.a_row0 + lrow0;                                      // slots
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -402,7 +420,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
       if (leader) mbar_expect_tx(&full_bar[s], 2 * kStageBytes);   // both CTAs' bytes
       const uint32_t fb = dsmem_addr(&full_bar[s], 0);
       tma_load_rows_pair(a, &tmap, (int64_t)(kb0 + kb) * kBK, kc, row0, fb);
-      tma_load_rows_pair(b, &tmap, (int64_t)(kb0 + kb) * kBK, kc, col0 + (int)cta * kTile, fb);
+      tma_load_rows_pair(b, &tmap, (int64_t)(kb0 + kb) * kBK, kc, blk.b_row0 + lcol0 + (int)cta * kTile, fb);
 #endif
     }
   } else if (warp == 1 && lane == 0 && leader) {
@@ -433,17 +451,19 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
   __syncwarp();
   mbar_wait(&done_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int i = row0 + warp * 32 + lane;
+  const int lr = lrow0 + warp * 32 + lane;
+  const int i = blk.a_key0 + lr;
   const int64_t nn = n;
 #pragma unroll 1
   for (int c = 0; c < kTile2; c += 32) {
     float r[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
-    if (i < n) {
+    if (lr < blk.a_cnt) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const int j = col0 + c + k;
-        if (j > i && j < n) {
+        const int lc = lcol0 + c + k;
+        const int j = blk.b_key0 + lc;
+        if (lc < blk.b_cnt && j > i) {
           const int64_t pid = (int64_t)i * (2 * nn - i - 1) / 2 + (j - i - 1);
           const double v = first ? (double)r[k] : out[pid] + (double)r[k];
           out[pid] = v;
@@ -540,6 +560,78 @@ rk_status ncc_compare(rk_app* app, const void* d_slots, size_t slot_stride, cons
   return RK_OK;
 }
 
+// K-chunked launches of the CTA-pair kernel over one Gram block
+rk_status gram_block_launch(rk_app* app, const CUtensorMap& map, const GramBlock& blk, double* d_out,
+                            uint8_t* d_flags, cudaStream_t s) {
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  const int tiles = blk.tri ? blk.na * (blk.na + 1) / 2 : blk.na * blk.nb;
+  const int mine = (tiles - blk.rank + blk.world - 1) / blk.world;
+  if (mine <= 0) return RK_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * mine);
+  cfg.blockDim = dim3(kGramThreads);
+  cfg.dynamicSmemBytes = gram_smem();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int kblocks = (int)(d / kBK);
+  for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkBlocks) {
+    const int kb1 = std::min(kblocks, kb0 + kChunkBlocks);
+    RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, app->p.n, d, app->ncc.kc, kb0, kb1, blk, d_out, d_flags,
+                               threshold_or_nan(app)));
+    app->launches += 1;
+  }
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+// the interleaved slot arena as a 4-D tensor map: (e % kc, slot % 128, e / kc, slot / 128)
+rk_status gram_tensor_map(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, CUtensorMap* map) {
+  const int64_t d = (int64_t)app->p.height * app->p.width;
+  if (slot_stride % 16 != 0) return set_error(RK_ERR_VALUE, "slot stride must be a multiple of 16 bytes");
+  if (n_rows % kGroup != 0)
+    return set_error(RK_ERR_VALUE, "Gram arena must hold whole slot groups of %d (got %d slots)", kGroup, n_rows);
+  EncodeTiledFn encode = nullptr;
+  RK_TRY(tensor_map_encoder(&encode));
+  const int64_t kc = app->ncc.kc;
+  const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)kGroup, (cuuint64_t)(d / kc), (cuuint64_t)(n_rows / kGroup)};
+  const cuuint64_t strides[3] = {(cuuint64_t)kc * 4, (cuuint64_t)kGroup * kc * 4, (cuuint64_t)kGroup * slot_stride};
+  const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)kTile, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult cr = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(d_slots), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  return RK_OK;
+}
+
+rk_status ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                         int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt, double* d_out,
+                         uint8_t* d_flags, cudaStream_t s) {
+  if (a_row0 % kGroup || b_row0 % kGroup)
+    return set_error(RK_ERR_VALUE, "Gram block rows must start on a slot group (%d)", kGroup);
+  if (a_cnt <= 0 || b_cnt <= 0 || a_row0 + a_cnt > n_rows || b_row0 + b_cnt > n_rows)
+    return set_error(RK_ERR_VALUE, "Gram block outside the arena");
+  if (a_key0 < 0 || b_key0 < 0 || a_key0 + a_cnt > app->p.n || b_key0 + b_cnt > app->p.n)
+    return set_error(RK_ERR_VALUE, "Gram block keys outside [0, n)");
+  const bool tri = a_row0 == b_row0 && a_key0 == b_key0 && a_cnt == b_cnt;
+  if (!tri && a_key0 + a_cnt > b_key0 && b_key0 + b_cnt > a_key0)
+    return set_error(RK_ERR_VALUE, "distinct Gram blocks must not overlap in keys");
+  if (!tri && a_key0 > b_key0)   // keep i < j: A is the lower key range
+    return ncc_gram_block(app, d_slots, slot_stride, n_rows, b_row0, b_key0, b_cnt, a_row0, a_key0, a_cnt, d_out,
+                          d_flags, s);
+  CUtensorMap map;
+  RK_TRY(gram_tensor_map(app, d_slots, slot_stride, n_rows, &map));
+  GramBlock blk{a_row0, a_key0, a_cnt, b_row0, b_key0, b_cnt, tri ? 1 : 0, 0, 1,
+                (a_cnt + kTile2 - 1) / kTile2, (b_cnt + kTile2 - 1) / kTile2};
+  return gram_block_launch(app, map, blk, d_out, d_flags, s);
+}
+
 rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t rank, int32_t world,
                    double* d_out, uint8_t* d_flags, cudaStream_t s) {
   const int64_t d = (int64_t)app->p.height * app->p.width;
@@ -564,32 +656,9 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
   if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 #ifndef NCC_GRAM_1CTA
   if (ncc_gram_tile(n) == kTile2) {
-    // CTA-pair kernel: 256x256 tiles, one cluster of 2 per tile
     const int side = (n + kTile2 - 1) / kTile2;
-    const int tiles = side * (side + 1) / 2;
-    const int mine = (tiles - rank + world - 1) / world;
-    if (mine <= 0) return RK_OK;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * mine);
-    cfg.blockDim = dim3(kGramThreads);
-    cfg.dynamicSmemBytes = gram_smem();
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const int kblocks = (int)(d / kBK);
-    for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkBlocks) {
-      const int kb1 = std::min(kblocks, kb0 + kChunkBlocks);
-      RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, n, d, kc, kb0, kb1, side, rank, world, d_out, d_flags,
-                                 threshold_or_nan(app)));
-      app->launches += 1;
-    }
-    RK_CUDA(cudaGetLastError());
-    return RK_OK;
+    GramBlock blk{0, 0, n, 0, 0, n, 1, rank, world, side, side};
+    return gram_block_launch(app, map, blk, d_out, d_flags, s);
   }
 #endif
   const int side = (n + kTile - 1) / kTile;

@@ -77,6 +77,14 @@ class DeviceApp:
                                   _ptr(flags), _stream(stream)))
 
 
+def ncc_gram_block(app: "DeviceApp", slots: torch.Tensor, n_rows: int, a_row0: int, a_key0: int, a_cnt: int,
+                   b_row0: int, b_key0: int, b_cnt: int, out: torch.Tensor, flags: Optional[torch.Tensor] = None,
+                   stream=None) -> None:
+    """One NCC Gram block (rk_ncc_gram_block) over an arena holding a subset of the items."""
+    check(lib.rk_ncc_gram_block(app.handle, _ptr(slots), app.slot_stride, n_rows, a_row0, a_key0, a_cnt, b_row0,
+                                b_key0, b_cnt, _ptr(out), _ptr(flags), _stream(stream)))
+
+
 def synth_prnu(h: int, w: int, first_key: int, n_items: int, cameras: int, seed: int,
                out: torch.Tensor, stream=None) -> torch.Tensor:
     """Deterministic PRNU-like fp32 patterns into `out` (device, n_items*h*w floats)."""

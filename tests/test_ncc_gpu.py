@@ -92,3 +92,36 @@ def test_constant_item_is_malformed():
     flat = torch.ones(64 * 64, dtype=torch.float32, device="cuda")
     with pytest.raises(MalformedInput):
         app.preprocess(flat, 64 * 64 * 4, 1, slots, [0])
+
+
+def test_gram_blocks_over_a_partial_arena():
+    """C3-style NCC: items split into key blocks placed anywhere in the arena (slot
+    groups of 128); the triangle of each block plus the rectangle between them
+    covers every pair exactly once and matches the oracle."""
+    _l, device = _mods()
+    n, side = 600, 256
+    d = side * side
+    items = make_items(n, side, seed=12)
+    app = device.DeviceApp(_l.app_params(_l.APP_NCC, n, height=side, width=side, threshold=0.02))
+    arena_rows = 768
+    slots = app.alloc_slots(arena_rows)
+    a_key0, a_cnt, a_row0 = 0, 256, 384          # keys 0..255 at slots 384..639
+    b_key0, b_cnt, b_row0 = 256, 344, 0          # keys 256..599 at slots 0..343
+    app.preprocess(items, d * 4, a_cnt, slots, list(range(a_row0, a_row0 + a_cnt)))
+    app.preprocess(items[b_key0 * d:], d * 4, b_cnt, slots, list(range(b_row0, b_row0 + b_cnt)))
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    device.ncc_gram_block(app, slots, arena_rows, a_row0, a_key0, a_cnt, a_row0, a_key0, a_cnt, out, flags)
+    device.ncc_gram_block(app, slots, arena_rows, b_row0, b_key0, b_cnt, b_row0, b_key0, b_cnt, out, flags)
+    # the rectangle, passed B-first: the ABI orders the blocks so that i < j
+    device.ncc_gram_block(app, slots, arena_rows, b_row0, b_key0, b_cnt, a_row0, a_key0, a_cnt, out, flags)
+    torch.cuda.synchronize()
+    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    got = out.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 2e-4
+    f = flags.cpu().numpy()
+    assert np.all((f == 1) | (f == 3)) and np.array_equal(f == 3, got >= 0.02)
+    with pytest.raises(ValueError):   # overlapping key ranges are not a valid block pair
+        device.ncc_gram_block(app, slots, arena_rows, 0, 0, 256, 384, 128, 256, out)
