@@ -2,7 +2,7 @@
 (256 GiB; no GPU holds them all) as a blocked tcgen05 Gram over the GPUs of one box.
 
   python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \\
-      --master-port 29700 tools/c3_ncc.py [--items 16384] [--side 2048] [--block 1024]
+      --master-port 29700 tools/c3_ncc.py [--items 16384] [--side 2048] [--block 2048]
 
 Items are split into key blocks of `block` items; block b lives on GPU
 owner(b) (serpentine over the ranks, so every rank gets the same triangle
@@ -10,7 +10,8 @@ work).  A rank computes the block pairs (I, J), I one of its home blocks and
 J >= I: home J in place, other J copied from the owner's arena over NVLink (CUDA
 IPC, double-buffered on a copy stream so the next block arrives while the
 current one is multiplied).  Each block pair is one rk_ncc_gram_block call
-(CTA-pair tcgen05 TF32 kernel, K-chunked).  The disjoint triangles are summed
+(CTA-pair tcgen05 TF32 kernel, K-chunked); the pairs of one J with the
+different home blocks run on their own streams, so together they fill the SMs.  The disjoint triangles are summed
 onto rank 0 with one NCCL reduce.  Reported: Gram time (max over ranks, CUDA
 events), pairs/s, TF32 TFLOP/s, bytes fetched, every pair written once, and
 sampled pairs against the fp32 per-pair path (|diff| <= 2e-4).
@@ -53,7 +54,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--items", type=int, default=16384)
     ap.add_argument("--side", type=int, default=2048)
-    ap.add_argument("--block", type=int, default=1024)
+    ap.add_argument("--block", type=int, default=2048)
     ap.add_argument("--cameras", type=int, default=256)
     ap.add_argument("--seed", type=int, default=5)
     ap.add_argument("--samples", type=int, default=16)
@@ -110,12 +111,15 @@ def main():
     out = torch.zeros(total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
     comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    lanes = [torch.cuda.Stream() for _ in home]            # one compute stream per home block
     fetched = [torch.cuda.Event(), torch.cuda.Event()]
-    used = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [[torch.cuda.Event() for _ in home] for _ in range(2)]
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
+    for ls in lanes:
+        ls.wait_stream(comp)
     nf, fetched_bytes, block_pairs = 0, 0, 0
     js = sorted({j for i in home for j in range(i, nblk)})
     for j in js:
@@ -125,22 +129,27 @@ def main():
         else:
             f = nf % 2
             if nf >= 2:
-                copy.wait_event(used[f])              # buffer f's previous block is done
+                for ev in used[f]:                    # buffer f's previous block is done
+                    copy.wait_event(ev)
             o = owner(j, world)
             src = peer[o] + home_of[o].index(j) * bs * stride
             check(lib.rk_memcpy_d2d(C.c_void_p(arena_p.value + fetch_rows[f] * stride), C.c_void_p(src),
                                     bs * stride, C.c_void_p(copy.cuda_stream)))
             fetched[f].record(copy)
-            comp.wait_event(fetched[f])
+            for ls in lanes:
+                ls.wait_event(fetched[f])
             jrow = fetch_rows[f]
             fetched_bytes += bs * stride
         for i in mine:
             device.ncc_gram_block(app, arena, n_rows, row_of_home[i], i * bs, bs, jrow, j * bs, bs, out, flags,
-                                  stream=comp)
+                                  stream=lanes[home.index(i)])
             block_pairs += 1
         if j not in row_of_home:
-            used[nf % 2].record(comp)
+            for k, ls in enumerate(lanes):
+                used[nf % 2][k].record(ls)
             nf += 1
+    for ls in lanes:
+        comp.wait_stream(ls)
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
