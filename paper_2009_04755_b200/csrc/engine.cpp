@@ -389,6 +389,72 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
 
 }  // namespace
 
+// NCC with fewer device slots than items: key blocks of B items (B = half the
+// arena, a multiple of the 256-item tile), block I in rows [0, B), block J in
+// rows [B, 2B); for every block pair I <= J dealt to this rank, the triangle of I
+// (J == I) or the I x J rectangle through rk_ncc_gram_block.  Block I is loaded
+// once per row of blocks, J once per pair (R ~ blocks / 2).
+rk_status ncc_blocked_run(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride,
+                          double* d_out, uint8_t* d_flags, int64_t launches0) {
+  const int32_t n = e->app->p.n;
+  const int32_t B = (int32_t)(e->arena_slots / 2) / 256 * 256;
+  if (B < 256)
+    return set_error(RK_ERR_NO_EVICTABLE, "blocked NCC Gram needs >= 512 device slots (have %zu)", e->arena_slots);
+  const int32_t nb = (n + B - 1) / B;
+  const size_t pbytes = e->app->parsed_bytes;
+  auto load_block = [&](int32_t blk, int32_t row0) -> rk_status {
+    const int32_t k0 = blk * B, cnt = std::min(n, k0 + B) - k0;
+    for (int32_t base = 0; base < cnt; base += e->staging_items) {
+      const int m = std::min(e->staging_items, cnt - base);
+      std::vector<int32_t> slots(m);
+      for (int q = 0; q < m; ++q) slots[q] = row0 + base + q;
+      if (h_parsed) {
+        for (int q = 0; q < m; ++q) {
+          RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->staging) + (size_t)q * pbytes,
+                                  static_cast<const char*>(h_parsed) + (size_t)(k0 + base + q) * parsed_stride, pbytes,
+                                  cudaMemcpyHostToDevice, e->stream));
+          e->stats.h2d_bytes += (int64_t)pbytes;
+        }
+        RK_TRY(rk_preprocess(e->app, e->staging, pbytes, m, e->arena, e->slot_stride, slots.data(), e->stream));
+      } else {
+        RK_TRY(rk_preprocess(e->app, static_cast<const char*>(d_parsed) + (size_t)(k0 + base) * parsed_stride,
+                             parsed_stride, m, e->arena, e->slot_stride, slots.data(), e->stream));
+      }
+      e->stats.loads += m;
+      e->stats.misses += m;
+    }
+    return RK_OK;
+  };
+  int64_t t = 0;
+  for (int32_t bi = 0; bi < nb; ++bi) {
+    bool loaded_i = false;
+    for (int32_t bj = bi; bj < nb; ++bj, ++t) {
+      if (t % e->p.world != e->p.rank) continue;
+      if (!loaded_i) {
+        RK_TRY(load_block(bi, 0));
+        loaded_i = true;
+      }
+      const int32_t ki = bi * B, ci = std::min(n, ki + B) - ki;
+      const int32_t kj = bj * B, cj = std::min(n, kj + B) - kj;
+      if (bj == bi) {
+        RK_TRY(rk_ncc_gram_block(e->app, e->arena, e->slot_stride, (int32_t)e->arena_slots, 0, ki, ci, 0, ki, ci, d_out,
+                                 d_flags, e->stream));
+        e->stats.pairs_done += (int64_t)ci * (ci - 1) / 2;
+      } else {
+        RK_TRY(load_block(bj, B));
+        RK_TRY(rk_ncc_gram_block(e->app, e->arena, e->slot_stride, (int32_t)e->arena_slots, 0, ki, ci, B, kj, cj, d_out,
+                                 d_flags, e->stream));
+        e->stats.pairs_done += (int64_t)ci * cj;
+      }
+      e->stats.tiles += 1;
+    }
+  }
+  RK_CUDA(cudaStreamSynchronize(e->stream));
+  RK_TRY(trace_collect(e));
+  e->stats.kernel_launches += e->app->launches - launches0;
+  return RK_OK;
+}
+
 extern "C" {
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params, int device,
@@ -509,8 +575,7 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   if (e->app->p.kind == RK_APP_NCC) {
     // Gram path: every item resident in slot == key, then one tcgen05 GEMM over
     // this rank's upper-triangle tiles
-    if (e->tier->capacity < n)
-      return set_error(RK_ERR_NO_EVICTABLE, "NCC Gram path needs device_slots >= n (%d < %d)", e->tier->capacity, n);
+    if (e->tier->capacity < n) return ncc_blocked_run(e, h_parsed, d_parsed, parsed_stride, d_out, d_flags, launches0);
     std::vector<LoadReq> all;
     for (int32_t k = 0; k < n; ++k) {
       const TierResult r = e->tier->acquire(k);

@@ -125,3 +125,32 @@ def test_gram_blocks_over_a_partial_arena():
     assert np.all((f == 1) | (f == 3)) and np.array_equal(f == 3, got >= 0.02)
     with pytest.raises(ValueError):   # overlapping key ranges are not a valid block pair
         device.ncc_gram_block(app, slots, arena_rows, 0, 0, 256, 384, 128, 256, out)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_engine_blocked_gram_when_items_exceed_slots(world):
+    """device_slots < n: the engine runs the Gram over key blocks that fit (half the
+    arena each), loading blocks as needed; ranks take block pairs round-robin."""
+    _l, device = _mods()
+    n, side = 600, 128
+    items = make_items(n, side, seed=14)
+    total = n * (n - 1) // 2
+    acc = torch.zeros(total, dtype=torch.float64, device="cuda")
+    fl = torch.zeros(total, dtype=torch.int32, device="cuda")
+    done = loads = 0
+    for rank in range(world):
+        eng = device.DeviceEngine(_l.app_params(_l.APP_NCC, n, height=side, width=side, threshold=0.02),
+                                  device_slots=512, rank=rank, world=world)
+        out = torch.zeros(total, dtype=torch.float64, device="cuda")
+        flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+        eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+        acc += out
+        fl += flags.to(torch.int32)
+        st = eng.stats()
+        done += st["pairs_done"]
+        loads += st["loads"]
+    assert done == total and loads > n            # blocks reloaded: R > 1
+    f = fl.cpu().numpy()
+    assert np.all((f == 1) | (f == 3))             # every pair exactly once
+    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    assert np.max(np.abs(acc.cpu().numpy() - want)) <= 2e-4
