@@ -233,3 +233,34 @@ def test_cv_large_skewed_items_match_oracle():
             assert abs(got[pid] - want) <= 1e-12 * max(1.0, abs(want)), (i, j, got[pid], want)
             pid += 1
     assert got[5 * (2 * n - 5 - 1) // 2 + 0] == pytest.approx(1.0, abs=1e-12)   # identical items 5, 6
+
+
+def test_exactly_once_over_random_runs():
+    """The reference's release criterion "every pair exactly once" over randomized
+    runs (test_acceptance.py:56-86): random n, leaf size, tier capacity and rank
+    count; the ranks' static shares together write each pair id once, and the
+    synthetic values are bit-exact with the reference's mix64 (oracle/rng.py)."""
+    from oracle import rng as orng
+    _l, device = _mods()
+    r = np.random.default_rng(2024)
+    for _ in range(40):
+        n = int(r.integers(2, 90))
+        leaf = int(r.integers(1, 12))
+        world = int(r.integers(1, 4))
+        seed = int(r.integers(0, 2**63))
+        total = n * (n - 1) // 2
+        cover = torch.zeros(total, dtype=torch.int32, device="cuda")
+        vals = torch.zeros(total, dtype=torch.float64, device="cuda")
+        for rank in range(world):
+            eng = device.DeviceEngine(_l.app_params(_l.APP_SYNTHETIC, n, seed=seed), leaf_block=leaf,
+                                      device_slots=int(r.integers(2, n + 2)), rank=rank, world=world)
+            out = torch.zeros(total, dtype=torch.float64, device="cuda")
+            flags = torch.full((total,), 255, dtype=torch.uint8, device="cuda")
+            eng.run(out, flags)
+            touched = flags != 255
+            cover += touched.to(torch.int32)
+            vals += torch.where(touched, out, torch.zeros_like(out))
+            eng.close()
+        assert bool((cover == 1).all()), (n, leaf, world)
+        want = np.array([orng.synthetic_value(seed, i, j) for i in range(n) for j in range(i + 1, n)])
+        assert np.array_equal(vals.cpu().numpy(), want), (n, leaf, world, seed)
