@@ -55,6 +55,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-steal", action="store_true", help="N > 1: static leaf shares, no cross-GPU stealing")
+    ap.add_argument("--trace-dir", default="",
+                    help="pce: after the timed steps, run one traced step and write the reference-schema "
+                         "trace (JSONL) and run-metrics document of each rank here")
     ap.add_argument("--app", default="pce", choices=["pce", "gmm", "cv"],
                     help="pce: configs[1] (default); gmm: configs[3]; cv: configs[4]")
     ap.add_argument("--angles", type=int, default=36, help="gmm: rotation grid K")
@@ -596,6 +599,35 @@ def main():
                    "peer_bytes_per_step": int(st2.get("peer_bytes", 0) // max(1, args.steps))}
         except RuntimeError as exc:  # e.g. pinned-memory exhaustion
             e2e = {"value": None, "unit": "pairs/s", "error": str(exc)[:200]}
+
+    if args.trace_dir:
+        # one extra (untimed) step with trace events: the reference's trace JSONL per
+        # rank and its RunMetrics document (metrics.py) with the perf-model efficiency
+        from paper_2009_04755_b200 import metrics as rk_metrics
+        from paper_2009_04755_b200 import perfmodel
+        os.makedirs(args.trace_dir, exist_ok=True)
+        eng.set_trace(200000)
+        eng.reset_stats()
+        step()
+        ev = eng.trace(node=rank)
+        eng.set_trace(0)
+        rk_metrics.write_trace(os.path.join(args.trace_dir, f"trace_rank{rank}.jsonl"), ev)
+        span = (max(e["end_ns"] for e in ev) - min(e["start_ns"] for e in ev)) / 1e9 if ev else 0.0
+        node = rk_metrics.node_metrics(rank, eng.stats(), span, n, ev)
+        comp = [e for e in ev if e["label"] == "compare"]
+        pre = [e for e in ev if e["label"] == "preprocess"]
+        t_cmp = sum(e["end_ns"] - e["start_ns"] for e in comp) / 1e9 / max(1, sum(e["count"] for e in comp))
+        t_pre = sum(e["end_ns"] - e["start_ns"] for e in pre) / 1e9 / max(1, sum(e["count"] for e in pre))
+        nodes = [(node, span, t_cmp, t_pre)]
+        if world > 1:
+            nodes = [None] * world
+            dist.all_gather_object(nodes, (node, span, t_cmp, t_pre))
+        if rank == 0:
+            costs = perfmodel.StageCosts(t_preprocess=max(x[3] for x in nodes), t_comparison=max(x[2] for x in nodes))
+            doc = rk_metrics.run_metrics({"workload": workload, "n": n, "side": side, "leaf_block": args.leaf,
+                                          "world": world}, n, [x[0] for x in nodes], max(x[1] for x in nodes),
+                                         costs=costs)
+            rk_metrics.write_metrics(os.path.join(args.trace_dir, "metrics.json"), doc)
 
     if rank != 0:
         if world > 1:
