@@ -3,10 +3,17 @@
 //
 // The driver is one host thread per GPU that enqueues everything on CUDA
 // streams, so the tier's WRITE state never blocks: a slot is published as
-// soon as its preprocess is enqueued, and stream order makes the data visible
-// to every later compare.  Eviction may overwrite a slot only after every
-// compare that reads it has been enqueued (pending pairs are flushed first),
-// which is the reference's lease rule (engine.py:530-534) in stream order.
+// soon as its load is enqueued.  Loads (H2D + preprocess, peer fetches) run on
+// a load stream and compares on the engine stream; events order them: a
+// compare batch waits for the loads issued before it, a load into an evicted
+// slot waits for every compare launched before the eviction -- the reference's
+// lease rule (engine.py:530-534) in stream order.
+//
+// Multi-GPU (one engine per rank): the peer-GPU tier (home GPU k mod world,
+// CUDA IPC mappings of the other ranks' arenas) and the cross-GPU work queue
+// (hierarchical stealing with system-scope atomics on per-rank queue words).
+// NCC runs as a tcgen05 Gram instead of per-pair launches: all items resident,
+// or key blocks of half the arena when the slots are fewer than the items.
 #include <math.h>
 #include <string.h>
 
