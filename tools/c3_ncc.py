@@ -58,6 +58,8 @@ def main():
     ap.add_argument("--cameras", type=int, default=256)
     ap.add_argument("--seed", type=int, default=5)
     ap.add_argument("--samples", type=int, default=16)
+    ap.add_argument("--copy-streams", type=int, default=1,
+                    help="concurrent D2D copies per block fetch (measured: 1: 0.676 s, 2: 0.711 s, 4: 0.707 s)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -110,9 +112,10 @@ def main():
     total = n * (n - 1) // 2
     out = torch.zeros(total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
-    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    comp = torch.cuda.Stream()
+    copies = [torch.cuda.Stream() for _ in range(args.copy_streams)]
     lanes = [torch.cuda.Stream() for _ in home]            # one compute stream per home block
-    fetched = [torch.cuda.Event(), torch.cuda.Event()]
+    fetched = [[torch.cuda.Event() for _ in copies] for _ in range(2)]
     used = [[torch.cuda.Event() for _ in home] for _ in range(2)]
     dist.barrier()
     torch.cuda.synchronize()
@@ -128,16 +131,21 @@ def main():
             jrow = row_of_home[j]
         else:
             f = nf % 2
-            if nf >= 2:
-                for ev in used[f]:                    # buffer f's previous block is done
-                    copy.wait_event(ev)
             o = owner(j, world)
             src = peer[o] + home_of[o].index(j) * bs * stride
-            check(lib.rk_memcpy_d2d(C.c_void_p(arena_p.value + fetch_rows[f] * stride), C.c_void_p(src),
-                                    bs * stride, C.c_void_p(copy.cuda_stream)))
-            fetched[f].record(copy)
+            dst = arena_p.value + fetch_rows[f] * stride
+            piece = (bs * stride) // len(copies)
+            for q, cs in enumerate(copies):           # the block in len(copies) concurrent pieces
+                if nf >= 2:
+                    for ev in used[f]:                # buffer f's previous block is done
+                        cs.wait_event(ev)
+                nbytes = piece if q < len(copies) - 1 else bs * stride - piece * q
+                check(lib.rk_memcpy_d2d(C.c_void_p(dst + q * piece), C.c_void_p(src + q * piece), nbytes,
+                                        C.c_void_p(cs.cuda_stream)))
+                fetched[f][q].record(cs)
             for ls in lanes:
-                ls.wait_event(fetched[f])
+                for ev in fetched[f]:
+                    ls.wait_event(ev)
             jrow = fetch_rows[f]
             fetched_bytes += bs * stride
         for i in mine:
@@ -186,7 +194,7 @@ def main():
             "tf32_tflops_useful": flop / (ms_max / 1e3) / 1e12,
             "tf32_tflops_useful_per_gpu": flop / (ms_max / 1e3) / 1e12 / world,
             "preprocess_s_max_rank": pre_max, "block_pairs": int(c[1].item()),
-            "fetched_gib": c[0].item() / 2**30,
+            "fetched_gib": c[0].item() / 2**30, "copy_streams": args.copy_streams,
             "check": {"flags_all_written_once": once, "sampled_pairs": len(pairs),
                       "max_abs_diff_vs_fp32_pairs_path": err}}), flush=True)
     for p in peer.values():
