@@ -7,6 +7,7 @@ repository snapshot.
 
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import shutil
 import subprocess
@@ -45,13 +46,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,
                      "-I", os.path.join(HERE, "..", "include")]
     common += os.environ.get("RK_NVCC_FLAGS", "").split()
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         cmd = [nvcc] + common + ["-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
-        subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units are independent: compile them concurrently
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.run, c, check=True, stdout=None if verbose else subprocess.DEVNULL)
+                  for c in cmds]:
+            f.result()
     tmp = LIB + ".tmp"
     subprocess.run([nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"], check=True)
     os.replace(tmp, LIB)

@@ -12,7 +12,12 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and runs the CUDA path")
     config.addinivalue_line("markers", "slow: long-running")
     # librocket.so must exist before the package is imported anywhere
-    from paper_2009_04755_b200 import _build
+    # (loaded by path: importing the package would need the library already built)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_rk_build", os.path.join(ROOT, "paper_2009_04755_b200", "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)
     _build.build()
 
 
