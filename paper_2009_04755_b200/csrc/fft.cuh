@@ -20,6 +20,26 @@
 
 namespace rk {
 
+// Complex arithmetic on packed fp32 pairs.  sm_100a issues one FADD2 / FMUL2 /
+// FFMA2 for both halves of a float2 and encodes scalar broadcast, half swap and
+// partial negation as operand modifiers, so a complex add is one instruction and
+// a complex multiply two (instead of two and four scalar ones).  -DRK_F32X2=0
+// restores the scalar forms (identical results up to FMA contraction order).
+#ifndef RK_F32X2
+#define RK_F32X2 1
+#endif
+#if RK_F32X2
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+}
+// a * conj(b) = b.x * a - b.y * (-a.y, a.x)
+__device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
+  return __ffma2_rn(make_float2(-b.y, -b.y), make_float2(-a.y, a.x), __fmul2_rn(make_float2(b.x, b.x), a));
+}
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+#else
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
@@ -29,8 +49,9 @@ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
 // (cos, sin)(2*pi*m/32) for m in [0, 16); m is a compile-time constant after unrolling.
 __device__ __forceinline__ float2 unit32(int m) {
@@ -140,6 +161,63 @@ struct Log2<1> {
   static constexpr int value = 0;
 };
 
+#if RK_F32X2
+// Radix-2 decimation-in-time butterfly with a compile-time twiddle W = W_32^m
+// (W = exp(-+2*pi*i/32)):  a <- a + W b,  b <- a - W b.  W b is factored as
+// c * (b + tau * i b) with |tau| <= 1 (tau = s/c, or the mirrored form when |s| > |c|),
+// so a general butterfly is three FFMA2 and a trivial one (m = 0, 8) two FADD2.
+template <bool INV>
+__device__ __forceinline__ void bfly_dit(float2& a, float2& b, int m) {
+  if (m == 0) {
+    const float2 t = b;
+    b = c_sub(a, t);
+    a = c_add(a, t);
+    return;
+  }
+  if (m == 8) {   // W = -i (forward) / +i (inverse)
+    const float2 t = INV ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
+    b = c_sub(a, t);
+    a = c_add(a, t);
+    return;
+  }
+  float2 w = unit32(m);
+  if (!INV) w.y = -w.y;
+  const float2 ib = make_float2(-b.y, b.x);   // i * b
+  float2 u;
+  float sc;
+  if (fabsf(w.x) >= fabsf(w.y)) {   // W b = c (b + (s/c) i b)
+    const float tau = w.y / w.x;
+    u = __ffma2_rn(make_float2(tau, tau), ib, b);
+    sc = w.x;
+  } else {                          // W b = s ((c/s) b + i b)
+    const float kap = w.x / w.y;
+    u = __ffma2_rn(make_float2(kap, kap), b, ib);
+    sc = w.y;
+  }
+  b = __ffma2_rn(make_float2(-sc, -sc), u, a);
+  a = __ffma2_rn(make_float2(sc, sc), u, a);
+}
+
+// In-register DFT of size N <= 32 (radix-2 decimation in time on the
+// bit-reversed input; the permutations are register renames), natural order in and out.
+template <int N, bool INV>
+__device__ __forceinline__ void dft_regs(float2 (&v)[N]) {
+  static_assert(N >= 2 && N <= 32 && (N & (N - 1)) == 0, "register DFT size");
+  float2 t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) t[i] = v[bitrev_const(i, Log2<N>::value)];
+#pragma unroll
+  for (int span = 1; span < N; span <<= 1) {
+#pragma unroll
+    for (int start = 0; start < N; start += 2 * span) {
+#pragma unroll
+      for (int k = 0; k < span; ++k) bfly_dit<INV>(t[start + k], t[start + k + span], k * (32 / (2 * span)));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = t[i];
+}
+#else
 // In-register DFT of size N <= 32 (radix-2 decimation in frequency), natural order in and out.
 template <int N, bool INV>
 __device__ __forceinline__ void dft_regs(float2 (&v)[N]) {
@@ -163,6 +241,7 @@ __device__ __forceinline__ void dft_regs(float2 (&v)[N]) {
 #pragma unroll
   for (int i = 0; i < N; ++i) v[i] = t[i];
 }
+#endif
 
 // Four-step N = R*R complex FFT over a group of R lanes (see file header).
 //   v     : lane's R elements, v[n2] = x[lane + R*n2] on entry, X[lane + R*k2] on exit
