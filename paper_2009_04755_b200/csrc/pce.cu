@@ -58,6 +58,12 @@ __host__ __device__ constexpr int cta_warps(int R) { return 4 * PCE_GROUPS / (32
 
 // Transpose buffer of the compare kernel: XOR-swizzled R*R (default) or padded
 // R*(R+1) for R = 32 (no per-element address registers; -DPCE_PAD_XPOSE=1).
+// Column-phase staging: per-warp slices and mbarriers (1) or one slice per warp
+// group refilled after a group barrier (0).
+#ifndef PCE_WARP_COLS
+#define PCE_WARP_COLS 1
+#endif
+
 #ifndef PCE_PAD_XPOSE
 #define PCE_PAD_XPOSE 0
 #endif
@@ -238,6 +244,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
   float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
   __shared__ __align__(8) uint64_t s_bar[kNG][3];   // per group: column slices, row block 0 / 1
   __shared__ __align__(8) uint64_t s_wbar;
+  __shared__ __align__(8) uint64_t s_cbar[kCtaWarps];   // per warp: its column slice (PCE_WARP_COLS)
   __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
   __shared__ float s_wpart[8];            // window energy per row pair, gathered in CTA 0
   __shared__ float s_v[kCtaWarps];
@@ -264,9 +271,11 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
     for (int w = 0; w < kNG; ++w)
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
     mbar_init(&s_wbar, 1);
+    for (int w = 0; w < kCtaWarps; ++w) mbar_init(&s_cbar[w], 1);
   }
   uint32_t ph = 0;                        // parity bits of this group's three barriers (bit b)
   uint32_t wph = 0;
+  uint32_t cph = 0;                       // parity of this warp's column-slice barrier (PCE_WARP_COLS)
   __syncthreads();
   const uint32_t part0 = dsmem_addr(&s_part[0], 0);
   const uint32_t wpart0 = dsmem_addr(&s_wpart[0], 0);
@@ -303,6 +312,28 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
     {
       const int cbeg = q * NCOL + 4 * wg, cend = (q + 1) * NCOL;
+#if PCE_WARP_COLS
+      // Per-warp pipeline: each warp owns the G columns of X and Y its lane groups
+      // transform, waits on its own mbarrier and refills its own slice as soon as its
+      // products are in registers -- no group barrier couples the four warps.
+      constexpr uint32_t kWarpBytes = (uint32_t)(G * N * sizeof(float2));
+      const int wcol = (warp % kGW) * G;            // first column of this warp within a slice
+      uint64_t* wbar = &s_cbar[warp];
+      float2* wx = gb + wcol * N;
+      float2* wy = gb + kHalf + wcol * N;
+      if (wl == 0) {
+        mbar_expect_tx(wbar, 2 * kWarpBytes);
+        bulk_g2s_hint(wx, Xs + (size_t)(cbeg + wcol) * N, kWarpBytes, wbar, pol_spec);
+        bulk_g2s_hint(wy, Ys + (size_t)(cbeg + wcol) * N, kWarpBytes, wbar, pol_spec);
+      }
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 4 * kNG) {
+        const int col = c0 + gi;
+        mbar_wait(wbar, cph & 1u);
+        cph ^= 1u;
+        const float2* X = gb + gi * N;
+        const float2* Y = gb + kHalf + gi * N;
+#else
       uint64_t* bar = &s_bar[wg][0];
       if (leader) {
         refill_fence();
@@ -317,6 +348,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
         ph ^= 1u;
         const float2* X = gb + gi * N;
         const float2* Y = gb + kHalf + gi * N;
+#endif
         if (col != 0) {
 #pragma unroll
           for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(X[lane + R * n2], Y[lane + R * n2]);
@@ -340,6 +372,14 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
             v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
           }
         }
+#if PCE_WARP_COLS
+        __syncwarp();                  // this warp's columns are consumed
+        if (wl == 0 && c0 + 4 * kNG < cend) {
+          mbar_expect_tx(wbar, 2 * kWarpBytes);
+          bulk_g2s_hint(wx, Xs + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);
+          bulk_g2s_hint(wy, Ys + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);
+        }
+#else
         named_bar(1 + wg, kGW * 32);   // this group's slices are consumed
         if (leader && c0 + 4 * kNG < cend) {
           refill_fence();
@@ -347,6 +387,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
           bulk_g2s_hint(gb, Xs + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
           bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
         }
+#endif
         compare_fft<R>(v, xbuf, twr, lane);
         // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
         const int rr = lane & 7;
