@@ -35,6 +35,15 @@
 
 #include <algorithm>
 
+// Scalar complex arithmetic in this kernel: with two 32-value FFT operands (e, o)
+// live at 255 registers, the packed-f32x2 DIT butterflies measured 61k vs 79k
+// pairs/s (same box, N = 512 at 2048^2).  -DPCE2K_F32X2=1 selects them.
+#ifndef PCE2K_F32X2
+#define PCE2K_F32X2 0
+#endif
+#ifndef RK_F32X2
+#define RK_F32X2 PCE2K_F32X2
+#endif
 #include "fft.cuh"
 #include "pce_common.cuh"
 #include "internal.h"
@@ -256,6 +265,13 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
   return warp_sum(w);
 }
 
+// Column-phase staging: per-warp columns and mbarriers (1) or one 4-column unit per
+// warp group refilled after a group barrier (0, default: 80.2k vs 74.4k pairs/s
+// same box at N = 512; the per-warp form wins at 1024^2, see pce.cu).
+#ifndef PCE2K_WARP_COLS
+#define PCE2K_WARP_COLS 0
+#endif
+
 __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, const char* __restrict__ slots,
                                                             size_t slot_stride, float2* __restrict__ T, size_t t_stride,
                                                             const float2* __restrict__ tw_g, double* __restrict__ out,
@@ -268,6 +284,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
   float2* xbufs = tw + R * R;                            // one padded transpose buffer per warp
   __shared__ __align__(8) uint64_t s_bar[2][3];          // per group: column units, row halves even / odd
   __shared__ __align__(8) uint64_t s_wbar;
+  __shared__ __align__(8) uint64_t s_cbar[kWarps];        // per warp: its column (PCE2K_WARP_COLS)
   __shared__ float s_v[kWarps];
   __shared__ int s_i[kWarps];
   __shared__ double s_ss[kWarps];
@@ -289,8 +306,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
     mbar_init(&s_wbar, 1);
+    for (int w = 0; w < kWarps; ++w) mbar_init(&s_cbar[w], 1);
   }
-  uint32_t ph = 0, wph = 0;
+  uint32_t ph = 0, wph = 0, cph = 0;
   __syncthreads();
   // hot-loop FFTs: lane twiddles in registers (default) or from the shared table
 #ifndef PCE2K_SMEM_TW
@@ -314,6 +332,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
     // unit u of this group: quartet wg + 2*(u >> 1), row parity u & 1
     {
       constexpr int kUnits = 2 * (kQuartets / 2);
+#if PCE2K_WARP_COLS
+      // per-warp pipeline: lane 0 copies this warp's own X and Y column of unit u
+      uint64_t* wbar = &s_cbar[warp];
+      auto issue = [&](int u) {
+        const int col = 4 * (wg + 2 * (u >> 1)) + gi, p = u & 1;
+        const size_t off = ((size_t)p * NC + col) * H;
+        constexpr uint32_t kColBytes = (uint32_t)(H * sizeof(float2));
+        refill_fence();
+        mbar_expect_tx(wbar, 2 * kColBytes);
+        bulk_g2s_hint(gb + gi * H, Xs + off, kColBytes, wbar, pol);
+        bulk_g2s_hint(gb + kUnitF2 + gi * H, Ys + off, kColBytes, wbar, pol);
+      };
+#else
       uint64_t* bar = &s_bar[wg][0];
       auto issue = [&](int u) {
         const int cq = wg + 2 * (u >> 1), p = u & 1;
@@ -323,12 +354,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         bulk_g2s_hint(gb, Xs + off, kUnitBytes, bar, pol);
         bulk_g2s_hint(gb + kUnitF2, Ys + off, kUnitBytes, bar, pol);
       };
+#endif
       // product X * conj(Y) of this warp's column for unit u, then refill the buffers
       auto product = [&](int u, float2 (&v)[R]) {
         const int col = 4 * (wg + 2 * (u >> 1)) + gi;
         const int p = u & 1;
+#if PCE2K_WARP_COLS
+        mbar_wait(wbar, cph & 1u);
+        cph ^= 1u;
+#else
         mbar_wait(bar, ph & 1u);
         ph ^= 1u;
+#endif
         const float2* X = gb + gi * H;
         const float2* Y = gb + kUnitF2 + gi * H;
         if (col != 0) {
@@ -354,10 +391,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
             v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
           }
         }
+#if PCE2K_WARP_COLS
+        __syncwarp();
+        if (lane == 0 && u + 1 < kUnits) issue(u + 1);
+      };
+      if (lane == 0) issue(0);
+#else
         named_bar(1 + wg, kGW * 32);
         if (leader && u + 1 < kUnits) issue(u + 1);
       };
       if (leader) issue(0);
+#endif
 #pragma unroll 1
       for (int u = 0; u < kUnits; u += 2) {
         const int col = 4 * (wg + 2 * (u >> 1)) + gi;

@@ -7,7 +7,7 @@ b "$B"; timeout 600 python -m pytest tests/test_pce_gpu.py -q -x > gpurun_out/${
 for r in 1 2; do
   for v in A B; do
     if [ $v = A ]; then b "$A"; else b "$B"; fi
-    timeout 600 python bench.py --items 2048 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_${v}${r}.log 2>&1
+    timeout 600 python bench.py ${BENCH_ARGS:---items 2048} --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_${v}${r}.log 2>&1
     python -c "import json,sys; d=json.loads(open('gpurun_out/${T}_${v}${r}.log').read().strip().splitlines()[-1]); print('$v$r', round(d['value']), d['roofline']['ms_per_launch'], d['clocks']['sm_mhz'], d['clocks']['reasons'])" | tee -a gpurun_out/${T}_summary.log
   done
 done
