@@ -308,7 +308,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
     mbar_init(&s_wbar, 1);
     for (int w = 0; w < kWarps; ++w) mbar_init(&s_cbar[w], 1);
   }
-  uint32_t ph = 0, wph = 0, cph = 0;
+  uint32_t ph = 0, wph = 0;
+#if PCE2K_WARP_COLS
+  uint32_t cph = 0;
+#endif
   __syncthreads();
   // hot-loop FFTs: lane twiddles in registers (default) or from the shared table
 #ifndef PCE2K_SMEM_TW
