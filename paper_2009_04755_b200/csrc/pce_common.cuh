@@ -26,6 +26,11 @@ __device__ __forceinline__ void refill_fence() {
   if (PCE_REFILL_FENCE) fence_proxy_async();
 }
 
+// Row-phase unpack and energy sums on packed pairs (with RK_F32X2).
+#ifndef PCE_X2_ROWS
+#define PCE_X2_ROWS 1
+#endif
+
 __device__ __forceinline__ bool better(float v, int idx, float bv, int bidx) {
   return v > bv || (v == bv && idx < bidx);
 }
@@ -64,7 +69,11 @@ __device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk,
       a = make_float2(n2 == 0 ? q.x : q.y, 0.f);
       c = make_float2(n2 == 0 ? q.z : q.w, 0.f);
     }
+#if PCE_X2_ROWS
+    v[n2] = c_add(a, make_float2(-c.y, c.x));   // a + i*c
+#else
     v[n2] = make_float2(a.x - c.y, a.y + c.x);
+#endif
   }
 }
 
@@ -102,12 +111,22 @@ template <int R>
 __device__ __forceinline__ void argmax_update(const float2 (&v)[R], int ra, int lane, float& m, int& idx, float& ss) {
   constexpr int N = R * R;
   float lm = -INFINITY;
+#if RK_F32X2 && PCE_X2_ROWS
+  float2 s2 = make_float2(0.f, 0.f);   // even / odd row sums, one FFMA2 per element
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) {
+    s2 = __ffma2_rn(v[k2], v[k2], s2);
+    lm = fmaxf(lm, fmaxf(v[k2].x, v[k2].y));
+  }
+  ss += s2.x + s2.y;
+#else
 #pragma unroll
   for (int k2 = 0; k2 < R; ++k2) {
     ss = fmaf(v[k2].x, v[k2].x, ss);
     ss = fmaf(v[k2].y, v[k2].y, ss);
     lm = fmaxf(lm, fmaxf(v[k2].x, v[k2].y));
   }
+#endif
   if (lm >= m) {
     int li = 0x7fffffff;
 #pragma unroll
