@@ -28,9 +28,19 @@ namespace rk {
 #ifndef RK_F32X2
 #define RK_F32X2 1
 #endif
+#ifndef RK_F32X2_MUL
+#define RK_F32X2_MUL RK_F32X2
+#endif
 #if RK_F32X2
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+#else
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
+#if RK_F32X2_MUL
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
   return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
 }
@@ -38,10 +48,7 @@ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
   return __ffma2_rn(make_float2(-b.y, -b.y), make_float2(-a.y, a.x), __fmul2_rn(make_float2(b.x, b.x), a));
 }
-__device__ __forceinline__ float2 c_scale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
 #else
-__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
@@ -49,7 +56,6 @@ __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 #endif
 __device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
 
@@ -161,7 +167,12 @@ struct Log2<1> {
   static constexpr int value = 0;
 };
 
-#if RK_F32X2
+// Register DFT structure: decimation in time with fused FFMA2 butterflies (1,
+// default with RK_F32X2) or the decimation-in-frequency form (0).
+#ifndef RK_DIT
+#define RK_DIT RK_F32X2
+#endif
+#if RK_DIT
 // Radix-2 decimation-in-time butterfly with a compile-time twiddle W = W_32^m
 // (W = exp(-+2*pi*i/32)):  a <- a + W b,  b <- a - W b.  W b is factored as
 // c * (b + tau * i b) with |tau| <= 1 (tau = s/c, or the mirrored form when |s| > |c|),

@@ -35,14 +35,23 @@
 
 #include <algorithm>
 
-// Scalar complex arithmetic in this kernel: with two 32-value FFT operands (e, o)
-// live at 255 registers, the packed-f32x2 DIT butterflies measured 61k vs 79k
-// pairs/s (same box, N = 512 at 2048^2).  -DPCE2K_F32X2=1 selects them.
+// Complex arithmetic in this kernel: packed FADD2 adds and the decimation-in-time
+// register DFT with FFMA2 butterflies, but scalar complex multiplies -- with two
+// 32-value FFT operands (e, o) live at 255 registers, building the swapped
+// operand of a packed multiply by a runtime twiddle costs more than it saves.
+// Same-box A/B at N = 512: all scalar (DIF) 78.2k, packed multiplies too 61.5k,
+// scalar + DIT 88.2k, packed adds + DIT 88.7k pairs/s (at a 110 MHz lower clock).
 #ifndef PCE2K_F32X2
-#define PCE2K_F32X2 0
+#define PCE2K_F32X2 1
 #endif
 #ifndef RK_F32X2
 #define RK_F32X2 PCE2K_F32X2
+#endif
+#ifndef RK_F32X2_MUL
+#define RK_F32X2_MUL 0
+#endif
+#ifndef RK_DIT
+#define RK_DIT 1
 #endif
 #include "fft.cuh"
 #include "pce_common.cuh"
