@@ -33,6 +33,7 @@
 
 #include <math.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -62,6 +63,14 @@ __host__ __device__ constexpr int cta_warps(int R) { return 4 * PCE_GROUPS / (32
 // group refilled after a group barrier (0).
 #ifndef PCE_WARP_COLS
 #define PCE_WARP_COLS 1
+#endif
+
+// Column-phase T stores (R = 32): the warp stages its column's 128 T segments
+// (8 KiB) in its transpose buffer and one lane issues a single TMA tensor store
+// (1), or every lane stores its 32 values with STG (0, default: the TMA form
+// measured 408k vs 418k pairs/s, same box, at a 20 MHz lower power-capped clock).
+#ifndef PCE_TMA_STORE
+#define PCE_TMA_STORE 0
 #endif
 
 #ifndef PCE_PAD_XPOSE
@@ -220,12 +229,26 @@ __device__ unsigned long long g_pce_probe[148 * 2 * 8];
   } while (0)
 #endif
 
+// TMA tensor store of one staged column of T (bulk group of the issuing thread).
+__device__ __forceinline__ void tma_store_col(const CUtensorMap* map, const void* src, int col, int cid) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+               ::"l"(map), "r"(0), "r"(col), "r"(0), "r"(cid), "r"(smem_u32(src)) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the source buffers of this thread's bulk stores may be overwritten
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// this thread's bulk stores are complete (visible in global memory)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <int R, int CL>
 __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster(
     const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
-    const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+    const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
+    const __grid_constant__ CUtensorMap tmap_T) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
+  constexpr bool kTmaStore = PCE_TMA_STORE && R == 32;
   constexpr int kCtaWarps = cta_warps(R);
   constexpr int NT = kCtaWarps * 32;
   constexpr int kNG = PCE_GROUPS;         // independent warp groups
@@ -388,14 +411,33 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
           bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
         }
 #endif
+        if (kTmaStore) {   // the previous column's store has read the transpose buffer
+          if (wl == 0) bulk_wait_read();
+          __syncwarp();
+        }
         compare_fft<R>(v, xbuf, twr, lane);
         // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
         const int rr = lane & 7;
         const int pos = (((rr >> 1) ^ ((col >> 1) & 3)) << 1) | (rr & 1);
-        float2* dst = Tp + ((size_t)(lane >> 3) * (N / 2) + col) * 8 + pos;
-        constexpr size_t kStep = (size_t)(R / 8) * (N / 2) * 8;
+        if (kTmaStore) {
+          // stage the column as T's 128 segments of 64 B ([block][8 rows], swizzled) in the
+          // (free) transpose buffer, then one tensor store writes all of them
+          float2* stg = xbuf + (lane >> 3) * 8 + pos;
 #pragma unroll
-        for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
+          for (int k2 = 0; k2 < R; ++k2) stg[k2 * (R / 8) * 8] = v[k2];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (wl == 0) tma_store_col(&tmap_T, xbuf, col, cid);
+        } else {
+          float2* dst = Tp + ((size_t)(lane >> 3) * (N / 2) + col) * 8 + pos;
+          constexpr size_t kStep = (size_t)(R / 8) * (N / 2) * 8;
+#pragma unroll
+          for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
+        }
+      }
+      if (kTmaStore) {   // T complete in global memory before the barrier; buffer reusable
+        if (wl == 0) bulk_wait_all();
+        __syncwarp();
       }
     }
     PCE_PROBE(1);
@@ -616,7 +658,7 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
   RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, st.t_stride, (const float2*)st.tw, d_out,
-                             d_flags, threshold_or_nan(app)));
+                             d_flags, threshold_or_nan(app), st.tmap_T));
   app->launches += 1;
   return RK_OK;
 }
@@ -634,6 +676,20 @@ rk_status cluster_init(rk_app* app) {
   st.clusters = clusters;
   st.t_stride = (size_t)(N / 2) * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * clusters));
+  memset(&st.tmap_T, 0, sizeof(st.tmap_T));
+  if (PCE_TMA_STORE && R == 32) {
+    // [cluster][8-row block][column][8 rows x complex64 = 16 floats]; box = one column
+    EncodeTiledFn encode = nullptr;
+    RK_TRY(tensor_map_encoder(&encode));
+    const cuuint64_t dims[4] = {16, (cuuint64_t)(N / 2), (cuuint64_t)(N / 8), (cuuint64_t)clusters};
+    const cuuint64_t strides[3] = {64, (cuuint64_t)(N / 2) * 64, (cuuint64_t)st.t_stride * sizeof(float2)};
+    const cuuint32_t box[4] = {16, 1, (cuuint32_t)(N / 8), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult cr = encode(&st.tmap_T, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, st.T, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled (PCE T) failed (%d)", (int)cr);
+  }
   st.job = new PairJob();
   return RK_OK;
 }
