@@ -274,11 +274,12 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
   return warp_sum(w);
 }
 
-// Column-phase staging: per-warp columns and mbarriers (1) or one 4-column unit per
-// warp group refilled after a group barrier (0, default: 80.2k vs 74.4k pairs/s
-// same box at N = 512; the per-warp form wins at 1024^2, see pce.cu).
+// Column-phase staging: per-warp columns and mbarriers (1, default) or one 4-column
+// unit per warp group refilled after a group barrier (0).  Same box at N = 512:
+// with the scalar DIF FFT the group form won (80.2k vs 74.4k pairs/s); with the
+// DIT FFMA2 butterflies the per-warp form wins (90.1k vs 89.0k at a 75 MHz lower clock).
 #ifndef PCE2K_WARP_COLS
-#define PCE2K_WARP_COLS 0
+#define PCE2K_WARP_COLS 1
 #endif
 
 __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, const char* __restrict__ slots,
