@@ -2,6 +2,7 @@
 
   python tools/ncc_bench.py [n] [side]
 """
+import hashlib
 import json
 import os
 import sys
@@ -51,12 +52,15 @@ def main():
         dapp.handle, base, stride.value, (_lib.Pair * len(sample))(*[_lib.Pair(i, j, i, j) for i, j in sample]),
         len(sample), ref.data_ptr(), None, torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    g = out.cpu().numpy()[pids]
+    out_h = out.cpu().numpy()
+    g = out_h[pids]
     f = ref.cpu().numpy()[pids]
     print(json.dumps({"n": n, "side": side, "pairs": total, "gram_ms": ms, "pairs_per_s": total / (ms / 1e3),
                       "tf32_tflops_issued": flops_tiles / (ms * 1e-3) / 1e12,
                       "tf32_tflops_useful": flops_pairs / (ms * 1e-3) / 1e12,
-                      "max_abs_err_vs_fp32": float(np.max(np.abs(g - f))), "sample": len(sample)}))
+                      "max_abs_err_vs_fp32": float(np.max(np.abs(g - f))), "sample": len(sample),
+                      "out_sha256": hashlib.sha256(out_h.tobytes()).hexdigest()[:16],
+                      "pdl": os.environ.get("RK_NCC_PDL", "1") != "0"}))
 
 
 if __name__ == "__main__":
