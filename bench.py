@@ -270,7 +270,7 @@ def main_app(args, rank, world, local_rank):
             cb = cpu_baseline_app(args.app, n, args.seed, budget, args.angles, args.mean_nnz)
             vals.append(cb["value"])
         value = sum(vals[args.warmup:] or vals) / len(vals[args.warmup:] or vals)
-        print(json.dumps({"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": 0,
+        print(json.dumps({"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": args.gpus, "host_only": True,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * pairs_total / value,
                           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                           "data": "synthetic", "config": {"workload": workload, "n": n,
@@ -445,7 +445,7 @@ def main():
             steps.append(cb["value"])
         vals = steps[args.warmup:] or steps
         value = sum(vals) / len(vals)
-        line = {"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": 0,
+        line = {"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": args.gpus, "host_only": True,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * pairs_total / value,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
