@@ -334,9 +334,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
 
 constexpr int kTile2 = 256;   // items per CTA-pair tile side
 #ifndef NCC_KCHUNK
-#define NCC_KCHUNK 2048
+#define NCC_KCHUNK 4096   // k-blocks per launch; A/B (profiles/r1_ab_ncc_stages*.log): 1024 32.9 ms, 2048 29.1-29.6, 4096 26.8-29.0, 8192 27.6-28.4
 #endif
-constexpr int kChunkBlocks = NCC_KCHUNK;   // k-blocks (x 32 floats) per launch: 64K floats
+constexpr int kChunkBlocks = NCC_KCHUNK;   // k-blocks (x 32 floats) per launch: 128K floats
 
 // A Gram block: rows of A = slots a_row0 .. a_row0 + a_cnt - 1 holding items (keys)
 // a_key0 .., the same for B; tri = A and B are the same block (upper-triangle

@@ -59,8 +59,7 @@ def main():
                       "tf32_tflops_issued": flops_tiles / (ms * 1e-3) / 1e12,
                       "tf32_tflops_useful": flops_pairs / (ms * 1e-3) / 1e12,
                       "max_abs_err_vs_fp32": float(np.max(np.abs(g - f))), "sample": len(sample),
-                      "out_sha256": hashlib.sha256(out_h.tobytes()).hexdigest()[:16],
-                      "pdl": os.environ.get("RK_NCC_PDL", "1") != "0"}))
+                      "out_sha256": hashlib.sha256(out_h.tobytes()).hexdigest()[:16]}))
 
 
 if __name__ == "__main__":
