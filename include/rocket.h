@@ -41,7 +41,8 @@ typedef enum {
   RK_ERR_SLOT_OVERFLOW = 3, /* SlotOverflow (errors.py:12-13; apps.py:128-132) */
   RK_ERR_NO_EVICTABLE = 4,  /* NoEvictableSlot (errors.py:16-20; slotcache.py:276-277) */
   RK_ERR_DEVICE = 5,        /* AppError: a CUDA call or kernel failed (errors.py:4-5) */
-  RK_ERR_UNSUPPORTED = 6    /* parameter combination not built for sm_100a in this library */
+  RK_ERR_UNSUPPORTED = 6,   /* parameter combination not built for sm_100a in this library */
+  RK_ERR_DUPLICATE = 7      /* AssertionError: a pair completed twice (PairLedger.mark, scheduler.py:233-241) */
 } rk_status;
 
 /* Application kinds.  SYNTHETIC and CV restate the reference's two built-in
@@ -179,6 +180,8 @@ typedef struct {
   int64_t steals;          /* chunks this rank stole from other ranks' queues */
   int64_t pinned_at_end;   /* device slots still leased when the run returned (must be 0) */
   int64_t writing_at_end;  /* device slots still in WRITE when the run returned (must be 0) */
+  int64_t ledger_marked;   /* pair ids set in the engine's own ledger after the run (-1: ledger shared, see rk_engine_ledger) */
+  int64_t dup_marks;       /* duplicate completions seen by the engine's own ledger */
 } rk_engine_stats;
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,
@@ -235,6 +238,37 @@ rk_status rk_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 rk_status rk_ipc_handle(const void* d_ptr, uint8_t* out_handle64);
 rk_status rk_ipc_open(const uint8_t* handle64, int device, void** d_ptr);
 rk_status rk_ipc_close(void* d_ptr);
+/* Exactly-once ledger (PairLedger, scheduler.py:218-246): a C(n,2)-bit bitmap in
+ * device memory, set by every compare epilogue with a system-scope atomicOr.  A
+ * bit found already set counts a duplicate, and the run fails with
+ * RK_ERR_DUPLICATE (the reference's AssertionError "pair (i, j) completed
+ * twice"); `completed == total` is the reference's `full`.
+ * Single GPU: the engine's own ledger, cleared at the start of every run.
+ * Multi-GPU: rank 0's ledger is the job's (its region of the IPC-shared arena);
+ * every rank passes rank 0's mapped region to rk_engine_use_ledger once, rank 0
+ * calls rk_engine_ledger_reset before the pre-run barrier and reads
+ * rk_engine_ledger after the post-run barrier. */
+typedef struct {
+  int64_t total;           /* C(n,2) */
+  int64_t completed;       /* bits set */
+  int64_t dup_marks;       /* duplicate completions */
+  int64_t first_dup_pid;   /* first duplicate pair id, -1 if none */
+  int32_t full;            /* completed == total && dup_marks == 0 */
+  int32_t shared;          /* marks go to a (possibly remote) shared ledger */
+} rk_ledger_stats;
+/* Offset and size of this engine's ledger region inside its arena allocation
+ * (the allocation rk_engine_arena returns and rk_ipc_handle exports). */
+rk_status rk_engine_ledger_region(const rk_engine* eng, size_t* offset, size_t* bytes);
+/* Mark into the ledger region at d_region (own or a peer's mapped one) from now on. */
+rk_status rk_engine_use_ledger(rk_engine* eng, void* d_region);
+rk_status rk_engine_ledger_reset(rk_engine* eng);
+rk_status rk_engine_ledger(rk_engine* eng, rk_ledger_stats* out);
+/* Ledger for callers of rk_compare_pairs / rk_compare_tile without an engine:
+ * d_region of rk_ledger_bytes(n) bytes, zeroed by the caller; NULL turns it off. */
+size_t rk_ledger_bytes(int64_t n);
+rk_status rk_app_set_ledger(rk_app* app, void* d_region);
+rk_status rk_ledger_read(void* d_region, int64_t n, rk_ledger_stats* out);
+
 /* Sample CUDA-event timing of every `every`-th compare batch (0 = off), at most
  * max_samples per run, on the engine's stream. */
 rk_status rk_engine_set_profiling(rk_engine* eng, int every, int max_samples);

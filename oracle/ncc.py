@@ -28,3 +28,26 @@ def all_pairs(items: np.ndarray) -> np.ndarray:
     g = z @ z.T
     iu = np.triu_indices(n, k=1)
     return g[iu]
+
+
+def all_pairs_chunked(items: np.ndarray, chunk: int = 1 << 16) -> np.ndarray:
+    """``all_pairs`` for items[n, ...] too large to hold as one float64 matrix:
+    means and norms in float64, then the Gram accumulated in float64 over column
+    chunks of D (same definition, summation split into chunks)."""
+    n = items.shape[0]
+    x = items.reshape(n, -1)
+    d = x.shape[1]
+    mean = np.zeros(n)
+    sq = np.zeros(n)
+    for c0 in range(0, d, chunk):
+        mean += x[:, c0:c0 + chunk].astype(np.float64).sum(axis=1)
+    mean /= d
+    g = np.zeros((n, n))
+    for c0 in range(0, d, chunk):
+        z = x[:, c0:c0 + chunk].astype(np.float64) - mean[:, None]
+        sq += np.einsum("ij,ij->i", z, z)
+        g += z @ z.T
+    inv = 1.0 / np.sqrt(sq)
+    g = g * inv[:, None] * inv[None, :]
+    iu = np.triu_indices(n, k=1)
+    return g[iu]

@@ -51,3 +51,14 @@ def pair_id(n: int, i: int, j: int) -> int:
 
 def pair_count(n: int) -> int:
     return n * (n - 1) // 2
+
+
+def pair_from_id(n: int, pid: int) -> tuple[int, int]:
+    """Inverse of ``pair_id`` (row i holds n-1-i consecutive ids)."""
+    if not 0 <= pid < pair_count(n):
+        raise ValueError(f"pair id {pid} out of range for n={n}")
+    i = 0
+    while pid >= n - 1 - i:
+        pid -= n - 1 - i
+        i += 1
+    return i, i + 1 + pid

@@ -24,6 +24,7 @@ RK_ERR_SLOT_OVERFLOW = 3
 RK_ERR_NO_EVICTABLE = 4
 RK_ERR_DEVICE = 5
 RK_ERR_UNSUPPORTED = 6
+RK_ERR_DUPLICATE = 7
 
 APP_SYNTHETIC = 0
 APP_CV = 1
@@ -80,7 +81,17 @@ class EngineStats(C.Structure):
         ("steals", C.c_int64),
         ("pinned_at_end", C.c_int64),
         ("writing_at_end", C.c_int64),
+        ("ledger_marked", C.c_int64),
+        ("dup_marks", C.c_int64),
     ]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class LedgerStats(C.Structure):
+    _fields_ = [("total", C.c_int64), ("completed", C.c_int64), ("dup_marks", C.c_int64),
+                ("first_dup_pid", C.c_int64), ("full", C.c_int32), ("shared", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -131,6 +142,13 @@ SIGNATURES = [
     ("rk_engine_load_home_range", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32]),
     ("rk_engine_set_peer_homes", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("rk_engine_set_trace", C.c_int, [C.c_void_p, C.c_int32]),
+    ("rk_engine_ledger_region", C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    ("rk_engine_use_ledger", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("rk_engine_ledger_reset", C.c_int, [C.c_void_p]),
+    ("rk_engine_ledger", C.c_int, [C.c_void_p, C.POINTER(LedgerStats)]),
+    ("rk_ledger_bytes", C.c_size_t, [C.c_int64]),
+    ("rk_app_set_ledger", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("rk_ledger_read", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(LedgerStats)]),
     ("rk_engine_trace_get", C.c_int64, [C.c_void_p, C.c_void_p, C.c_int64]),
     ("rk_engine_peer_bandwidth", C.c_int, [C.c_void_p, C.c_int32, C.c_size_t, C.POINTER(C.c_double)]),
     ("rk_engine_queue_word", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
@@ -189,6 +207,8 @@ def check(status: int) -> None:
         raise NoEvictableSlot(msg)
     if status == RK_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if status == RK_ERR_DUPLICATE:
+        raise AssertionError(msg)      # PairLedger.mark (scheduler.py:233-241)
     raise AppError(f"librocket device failure: {msg}")
 
 

@@ -130,6 +130,7 @@ const char* rk_status_name(int status) {
     case RK_ERR_NO_EVICTABLE: return "RK_ERR_NO_EVICTABLE";
     case RK_ERR_DEVICE: return "RK_ERR_DEVICE";
     case RK_ERR_UNSUPPORTED: return "RK_ERR_UNSUPPORTED";
+    case RK_ERR_DUPLICATE: return "RK_ERR_DUPLICATE";
     default: return "RK_ERR_UNKNOWN";
   }
 }

@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PairJob job, cons
 
 __global__ void cv_finalize(const PairJob job, const uint8_t* __restrict__ slots, size_t slot_stride,
                             const int* __restrict__ offsets, const double* __restrict__ partial,
-                            double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+                            double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
+                            const LedgerRef ledger) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= job.npairs) return;
   double t = 0.0;
@@ -275,6 +276,7 @@ __global__ void cv_finalize(const PairJob job, const uint8_t* __restrict__ slots
   const double norm_b = *reinterpret_cast<const double*>(slots + (size_t)job.pairs[p].slot_b * slot_stride + 8);
   const double v = (norm_a > 0.0 && norm_b > 0.0) ? t / (norm_a * norm_b) : 0.0;
   out[job.pairs[p].pid] = v;
+  ledger_mark(ledger, job.pairs[p].pid);
   if (flags) flags[job.pairs[p].pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
 }
 
@@ -352,7 +354,7 @@ rk_status cv_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, 
     cv_work<<<app->cv_grid, kCvWarps * 32, 0, s>>>(job, slots, slot_stride, app->p.max_entries, offsets, ctl,
                                                    partial);
     cv_finalize<<<(m + 127) / 128, 128, 0, s>>>(job, slots, slot_stride, offsets, partial, d_out, d_flags,
-                                                threshold_or_nan(app));
+                                                threshold_or_nan(app), app->ledger);
     app->launches += 3;
     RK_CUDA(cudaGetLastError());
   }

@@ -152,6 +152,63 @@ __global__ void queue_op_kernel(unsigned long long* word, int op, unsigned long 
 }
 
 // ---------------------------------------------------------------------------
+// Exactly-once ledger region: C(n,2) bits (rounded up to 256 B), then 256 B of
+// counters (LedgerRef.ctr).  Lives in the engine's arena allocation so that the
+// same IPC handle that maps the home region maps it for the other ranks.
+size_t ledger_bits_bytes(int64_t n) {
+  const int64_t total = n > 1 ? n * (n - 1) / 2 : 0;
+  return (size_t)((total + 31) / 32 * 4 + 255) / 256 * 256;
+}
+size_t ledger_region_bytes(int64_t n) { return ledger_bits_bytes(n) + 256; }
+LedgerRef ledger_at(void* region, int64_t n) {
+  char* r = static_cast<char*>(region);
+  return LedgerRef{reinterpret_cast<uint32_t*>(r), reinterpret_cast<unsigned long long*>(r + ledger_bits_bytes(n))};
+}
+
+__global__ void ledger_count_kernel(const uint32_t* __restrict__ bits, int64_t words, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+    c += (unsigned long long)__popc(bits[w]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd_system(out, c);
+}
+
+// completed = popcount of the bitmap, plus the duplicate counters (synchronous on s)
+rk_status ledger_read(void* region, int64_t n, cudaStream_t s, rk_ledger_stats* out) {
+  const int64_t total = n > 1 ? n * (n - 1) / 2 : 0;
+  const LedgerRef L = ledger_at(region, n);
+  RK_CUDA(cudaMemsetAsync(L.ctr + 2, 0, sizeof(unsigned long long), s));
+  const int64_t words = (total + 31) / 32;
+  if (words > 0) {
+    const int blocks = (int)std::min<int64_t>(1184, (words + 255) / 256);
+    ledger_count_kernel<<<blocks, 256, 0, s>>>(L.bits, words, L.ctr + 2);
+    RK_CUDA(cudaGetLastError());
+  }
+  unsigned long long h[3] = {0, 0, 0};
+  RK_CUDA(cudaMemcpyAsync(h, L.ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  out->total = total;
+  out->completed = (int64_t)h[2];
+  out->dup_marks = (int64_t)h[0];
+  out->first_dup_pid = h[1] ? (int64_t)h[1] - 1 : -1;
+  out->full = out->completed == total && out->dup_marks == 0;
+  out->shared = 0;
+  return RK_OK;
+}
+
+rk_status duplicate_error(int64_t n, const rk_ledger_stats& ls) {
+  int64_t i = 0, j = 0, pid = ls.first_dup_pid;
+  while (pid >= n - 1 - i) {
+    pid -= n - 1 - i;
+    ++i;
+  }
+  j = i + 1 + pid;
+  return set_error(RK_ERR_DUPLICATE, "pair (%lld, %lld) completed twice (%lld duplicate marks)", (long long)i,
+                   (long long)j, (long long)ls.dup_marks);
+}
+
+// ---------------------------------------------------------------------------
 // Slot tier (CacheTier restated, slotcache.py:139-282)
 SlotTier::SlotTier(int cap) : capacity(cap) {
   key.assign(cap, -1);
@@ -278,6 +335,13 @@ struct rk_engine {
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_pairs;
   int ev_used = 0;
+  // exactly-once ledger: own region in the arena allocation; marks go to `ledger_target`
+  // (own, or rank 0's region mapped over IPC when the job shares one ledger)
+  size_t ledger_off = 0;
+  size_t ledger_bytes = 0;
+  void* ledger_own = nullptr;
+  void* ledger_target = nullptr;
+  bool ledger_shared = false;
 };
 
 using namespace rk;
@@ -500,10 +564,16 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   const size_t g = (size_t)std::max(1, e->app->slot_group);
   e->arena_slots = ((size_t)params->device_slots + g - 1) / g * g;
   const size_t arena_bytes = e->slot_stride * (e->arena_slots + e->home_slots);
-  ce = cudaMalloc(&e->arena, arena_bytes + 256);   // + the work-queue word (shared with the home region over IPC)
+  // + the work-queue word and the ledger region (shared with the home region over IPC)
+  e->ledger_off = arena_bytes + 256;
+  e->ledger_bytes = ledger_region_bytes(app_params->n);
+  ce = cudaMalloc(&e->arena, arena_bytes + 256 + e->ledger_bytes);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(slot arena)"));
   e->qword = reinterpret_cast<unsigned long long*>(static_cast<char*>(e->arena) + arena_bytes);
-  ce = cudaMemset(e->qword, 0, 256);
+  e->ledger_own = static_cast<char*>(e->arena) + e->ledger_off;
+  e->ledger_target = e->ledger_own;
+  e->app->ledger = ledger_at(e->ledger_own, app_params->n);
+  ce = cudaMemset(e->qword, 0, 256 + e->ledger_bytes);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaHostAlloc(&e->h_qres, 64, cudaHostAllocMapped);
   if (ce == cudaSuccess) ce = cudaHostGetDevicePointer(&e->d_qres, e->h_qres, 0);
@@ -555,9 +625,32 @@ rk_status rk_engine_set_profiling(rk_engine* e, int every, int max_samples) {
   return RK_OK;
 }
 
+static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride,
+                                 double* d_out, uint8_t* d_flags);
+
+// Every run marks each completed pair in the ledger; a duplicate fails the run
+// (PairLedger.mark's AssertionError).  A private ledger is cleared and checked
+// here; a shared one (multi-GPU) by rank 0 around the job's barriers.
 rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride, double* d_out,
                         uint8_t* d_flags) {
   if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  RK_CUDA(cudaSetDevice(e->device));
+  if (!e->ledger_shared) RK_CUDA(cudaMemsetAsync(e->ledger_own, 0, e->ledger_bytes, e->stream));
+  RK_TRY(engine_run_impl(e, h_parsed, d_parsed, parsed_stride, d_out, d_flags));
+  if (e->ledger_shared) {
+    e->stats.ledger_marked = -1;
+    return RK_OK;
+  }
+  rk_ledger_stats ls{};
+  RK_TRY(ledger_read(e->ledger_own, e->app->p.n, e->stream, &ls));
+  e->stats.ledger_marked = ls.completed;
+  e->stats.dup_marks += ls.dup_marks;
+  if (ls.dup_marks) return duplicate_error(e->app->p.n, ls);
+  return RK_OK;
+}
+
+static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void* d_parsed, size_t parsed_stride,
+                                 double* d_out, uint8_t* d_flags) {
   if (!h_parsed && !d_parsed && e->app->p.kind != RK_APP_SYNTHETIC && e->home_slots == 0)
     return set_error(RK_ERR_VALUE, "need host or device parsed items");
   RK_CUDA(cudaSetDevice(e->device));
@@ -777,6 +870,51 @@ rk_status rk_engine_run(rk_engine* e, const void* h_parsed, const void* d_parsed
   e->stats.evictions = e->tier->evictions;
   e->stats.kernel_launches += e->app->launches - launches0;
   return RK_OK;
+}
+
+rk_status rk_engine_ledger_region(const rk_engine* e, size_t* offset, size_t* bytes) {
+  if (!e || !offset || !bytes) return set_error(RK_ERR_VALUE, "null argument");
+  *offset = e->ledger_off;
+  *bytes = e->ledger_bytes;
+  return RK_OK;
+}
+
+rk_status rk_engine_use_ledger(rk_engine* e, void* d_region) {
+  if (!e || !d_region) return set_error(RK_ERR_VALUE, "null argument");
+  e->ledger_target = d_region;
+  e->ledger_shared = true;
+  e->app->ledger = ledger_at(d_region, e->app->p.n);
+  return RK_OK;
+}
+
+rk_status rk_engine_ledger_reset(rk_engine* e) {
+  if (!e) return set_error(RK_ERR_VALUE, "null engine");
+  if (e->ledger_target != e->ledger_own) return RK_OK;   // the owner (rank 0) clears a shared ledger
+  RK_CUDA(cudaSetDevice(e->device));
+  RK_CUDA(cudaMemsetAsync(e->ledger_own, 0, e->ledger_bytes, e->stream));
+  RK_CUDA(cudaStreamSynchronize(e->stream));
+  return RK_OK;
+}
+
+rk_status rk_engine_ledger(rk_engine* e, rk_ledger_stats* out) {
+  if (!e || !out) return set_error(RK_ERR_VALUE, "null argument");
+  RK_CUDA(cudaSetDevice(e->device));
+  RK_TRY(ledger_read(e->ledger_target, e->app->p.n, e->cstream, out));
+  out->shared = e->ledger_shared ? 1 : 0;
+  return RK_OK;
+}
+
+size_t rk_ledger_bytes(int64_t n) { return ledger_region_bytes(n); }
+
+rk_status rk_app_set_ledger(rk_app* app, void* d_region) {
+  if (!app) return set_error(RK_ERR_VALUE, "null app");
+  app->ledger = d_region ? ledger_at(d_region, app->p.n) : LedgerRef{nullptr, nullptr};
+  return RK_OK;
+}
+
+rk_status rk_ledger_read(void* d_region, int64_t n, rk_ledger_stats* out) {
+  if (!d_region || !out) return set_error(RK_ERR_VALUE, "null argument");
+  return ledger_read(d_region, n, nullptr, out);
 }
 
 rk_status rk_engine_stats_get(const rk_engine* e, rk_engine_stats* out) {

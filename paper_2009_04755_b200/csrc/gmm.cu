@@ -183,13 +183,15 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob
 }
 
 __global__ void gmm_finalize(const PairJob job, int nblk, const double* __restrict__ blk_best,
-                             double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+                             double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
+                             const LedgerRef ledger) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= job.npairs) return;
   double v = -1.0;
   for (int b = 0; b < nblk; ++b) v = fmax(v, blk_best[(size_t)p * nblk + b]);
   const int64_t pid = job.pairs[p].pid;
   out[pid] = v;
+  ledger_mark(ledger, pid);
   if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
 }
 
@@ -248,7 +250,7 @@ rk_status gmm_compare_list(rk_app* app, const void* d_slots, size_t slot_stride,
     const int nblk = (app->p.gmm_angles + kAngBlock - 1) / kAngBlock;
     gmm_pair_kernel<<<m * nblk, kPairWarps * 32, smem, s>>>(job, static_cast<const uint8_t*>(d_slots), slot_stride,
                                                             app->p.gmm_angles, app->p.gmm_scale, app->gmm_scratch);
-    gmm_finalize<<<(m + 127) / 128, 128, 0, s>>>(job, nblk, app->gmm_scratch, d_out, d_flags, threshold_or_nan(app));
+    gmm_finalize<<<(m + 127) / 128, 128, 0, s>>>(job, nblk, app->gmm_scratch, d_out, d_flags, threshold_or_nan(app), app->ledger);
     app->launches += 2;
     RK_CUDA(cudaGetLastError());
   }

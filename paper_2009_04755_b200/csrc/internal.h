@@ -43,6 +43,46 @@ struct PairBatch {
   int64_t pid[kMaxBatch];
 };
 
+// Exactly-once ledger (PairLedger, scheduler.py:218-246) on the device: one bit
+// per pair id, set with a system-scope atomicOr in every compare epilogue (the
+// bitmap may live on another GPU of the box: the shared ledger of a multi-GPU
+// job sits on rank 0 and is marked over NVLink).  A bit that was already set is
+// a duplicate completion -- the reference's AssertionError: ctr[0] counts them,
+// ctr[1] holds the first duplicate pair id + 1.  bits == nullptr: no ledger.
+struct LedgerRef {
+  uint32_t* bits;
+  unsigned long long* ctr;   // [0] duplicate marks, [1] first duplicate pid + 1, [2] scratch (popcount)
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void ledger_mark(const LedgerRef& L, int64_t pid) {
+  if (L.bits == nullptr) return;
+  const uint32_t bit = 1u << (uint32_t)(pid & 31);
+  const uint32_t old = atomicOr_system(L.bits + (pid >> 5), bit);
+  if (old & bit) {
+    atomicAdd_system(L.ctr, 1ull);
+    atomicCAS_system(L.ctr + 1, 0ull, (unsigned long long)pid + 1ull);
+  }
+}
+// `cnt` consecutive pair ids from pid0 (a tile row's run of columns): one
+// atomicOr per 32-bit word instead of one per pair.
+__device__ __forceinline__ void ledger_mark_run(const LedgerRef& L, int64_t pid0, int cnt) {
+  if (L.bits == nullptr) return;
+  int64_t p = pid0;
+  while (cnt > 0) {
+    const int off = (int)(p & 31);
+    const int take = cnt < 32 - off ? cnt : 32 - off;
+    const uint32_t mask = (take == 32 ? 0xffffffffu : ((1u << take) - 1u)) << off;
+    const uint32_t dup = atomicOr_system(L.bits + (p >> 5), mask) & mask;
+    if (dup) {
+      atomicAdd_system(L.ctr, (unsigned long long)__popc(dup));
+      atomicCAS_system(L.ctr + 1, 0ull, (unsigned long long)((p & ~(int64_t)31) + __ffs(dup) - 1) + 1ull);
+    }
+    p += take;
+    cnt -= take;
+  }
+}
+#endif
+
 struct SlotList {
   int32_t n;
   int32_t idx[kMaxBatch];
@@ -102,6 +142,7 @@ struct rk_app {
   int cv_grid = 0;                  // persistent CV work grid (SMs x resident CTAs)
   rk::PceState pce;
   rk::NccState ncc;
+  rk::LedgerRef ledger{nullptr, nullptr};   // marked by every compare epilogue (null: off)
 };
 
 namespace rk {

@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(256) ncc_normalise(const float* __restrict__ p
 // per-pair path: one warp per pair, fp32 dot with float4 loads
 __global__ void __launch_bounds__(256) ncc_pairs_kernel(PairBatch b, const char* __restrict__ slots, size_t slot_stride,
                                                         int64_t d, int64_t kc, double* __restrict__ out,
-                                                        uint8_t* __restrict__ flags, double threshold) {
+                                                        uint8_t* __restrict__ flags, double threshold,
+                                                        const LedgerRef ledger) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * 8 + warp;
   if (p >= b.npairs) return;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(256) ncc_pairs_kernel(PairBatch b, const char*
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) {
     out[b.pid[p]] = acc;
+    ledger_mark(ledger, b.pid[p]);
     if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (acc >= threshold ? 2 : 0));
   }
 }
@@ -236,7 +238,8 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_constant__ CUtensorMap tmap, int n,
                                                                    int64_t d, int64_t kc, int tiles_per_side, int rank, int world,
                                                                    double* __restrict__ out,
-                                                                   uint8_t* __restrict__ flags, double threshold) {
+                                                                   uint8_t* __restrict__ flags, double threshold,
+                                                                   const LedgerRef ledger) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
@@ -324,6 +327,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram_kernel(const __grid_
           if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | ((double)r[k] >= threshold ? 2 : 0));
         }
       }
+      // the valid columns j of this run are contiguous, and so are their pair ids
+      const int j0 = max(col0 + c, i + 1), j1 = min(col0 + c + 32, n);
+      if (j1 > j0) ledger_mark_run(ledger, (int64_t)i * (2 * nn - i - 1) / 2 + (j0 - i - 1), j1 - j0);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -359,7 +365,8 @@ struct GramBlock {
 __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid_constant__ CUtensorMap tmap, int n,
                                                                     int64_t d, int64_t kc, int kb0, int kb1,
                                                                     const GramBlock blk, double* __restrict__ out,
-                                                                    uint8_t* __restrict__ flags, double threshold) {
+                                                                    uint8_t* __restrict__ flags, double threshold,
+                                                                    const LedgerRef ledger) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
@@ -470,6 +477,10 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
           if (flags && (int64_t)kb1 * kBK >= d) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
         }
       }
+      if ((int64_t)kb1 * kBK >= d) {   // the pairs complete with their last K chunk
+        const int l0 = max(lcol0 + c, i + 1 - blk.b_key0), l1 = min(lcol0 + c + 32, blk.b_cnt);
+        if (l1 > l0) ledger_mark_run(ledger, (int64_t)i * (2 * nn - i - 1) / 2 + (blk.b_key0 + l0 - i - 1), l1 - l0);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -554,7 +565,7 @@ rk_status ncc_compare(rk_app* app, const void* d_slots, size_t slot_stride, cons
   const int64_t d = (int64_t)app->p.height * app->p.width;
   ncc_pairs_kernel<<<(b.npairs + 7) / 8, 256, 0, s>>>(b, static_cast<const char*>(d_slots), slot_stride, d,
                                                        app->ncc.kc, d_out,
-                                                       d_flags, threshold_or_nan(app));
+                                                       d_flags, threshold_or_nan(app), app->ledger);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;
@@ -583,7 +594,7 @@ rk_status gram_block_launch(rk_app* app, const CUtensorMap& map, const GramBlock
   for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkBlocks) {
     const int kb1 = std::min(kblocks, kb0 + kChunkBlocks);
     RK_CUDA(cudaLaunchKernelEx(&cfg, ncc_gram2_kernel, map, app->p.n, d, app->ncc.kc, kb0, kb1, blk, d_out, d_flags,
-                               threshold_or_nan(app)));
+                               threshold_or_nan(app), app->ledger));
     app->launches += 1;
   }
   RK_CUDA(cudaGetLastError());
@@ -666,7 +677,7 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
   const int mine = (tiles - rank + world - 1) / world;
   if (mine <= 0) return RK_OK;
   ncc_gram_kernel<<<mine, kGramThreads, gram_smem(), s>>>(map, n, d, kc, side, rank, world, d_out, d_flags,
-                                                          threshold_or_nan(app));
+                                                          threshold_or_nan(app), app->ledger);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;

@@ -245,7 +245,7 @@ template <int R, int CL>
 __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster(
     const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
-    const __grid_constant__ CUtensorMap tmap_T) {
+    const __grid_constant__ CUtensorMap tmap_T, const LedgerRef ledger) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
   constexpr bool kTmaStore = PCE_TMA_STORE && R == 32;
@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
       const double energy = (s_total - wsum) / ((double)N * (double)N - (double)(kWin * kWin));
       const double pce = peak * fabs(peak) / energy;
       out[pr.pid] = pce;
+      ledger_mark(ledger, pr.pid);
       if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
     }
   }
@@ -658,7 +659,7 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
   RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, st.t_stride, (const float2*)st.tw, d_out,
-                             d_flags, threshold_or_nan(app), st.tmap_T));
+                             d_flags, threshold_or_nan(app), st.tmap_T, app->ledger));
   app->launches += 1;
   return RK_OK;
 }

@@ -285,7 +285,8 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
 __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, const char* __restrict__ slots,
                                                             size_t slot_stride, float2* __restrict__ T, size_t t_stride,
                                                             const float2* __restrict__ tw_g, double* __restrict__ out,
-                                                            uint8_t* __restrict__ flags, double threshold) {
+                                                            uint8_t* __restrict__ flags, double threshold,
+                                                            const LedgerRef ledger) {
   constexpr int kGW = kWarps / 2;                        // warps per warp group
   constexpr int kPairsOfRows = (kWin + 1) / 2;
   extern __shared__ __align__(128) float2 smem[];
@@ -534,6 +535,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
       const double energy = (s_total - wsum) / ((double)N * (double)N - (double)(kWin * kWin));
       const double pce = peak * fabs(peak) / energy;
       out[pr.pid] = pce;
+      ledger_mark(ledger, pr.pid);
       if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
     }
     __syncthreads();   // shared state and buffers free for the next pair
@@ -594,7 +596,7 @@ rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, cons
   }
   const int grid = std::min(st.clusters, n);
   pce2k_pair<<<grid, kWarps * 32, kPairSmem, s>>>(job, slots, slot_stride, st.T, st.t_stride, st.tw, d_out, d_flags,
-                                                   threshold_or_nan(app));
+                                                   threshold_or_nan(app), app->ledger);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;

@@ -29,18 +29,20 @@ namespace {
 // value = mix64(seed, 0xC0403A3E, i, j) / 2^64 ; Python converts the int to the
 // nearest double (ties to even) before the exact power-of-two division.
 __global__ void synth_compare_kernel(PairBatch b, uint64_t seed, double* __restrict__ out, uint8_t* __restrict__ flags,
-                                     double threshold) {
+                                     double threshold, const LedgerRef ledger) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= b.npairs) return;
   const uint64_t h = mix64_4(seed, 0xC0403A3Eull, (uint64_t)(int64_t)b.key_i[p], (uint64_t)(int64_t)b.key_j[p]);
   const double v = __ull2double_rn(h) * 0x1p-64;
   out[b.pid[p]] = v;
+  ledger_mark(ledger, b.pid[p]);
   if (flags) flags[b.pid[p]] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
 }
 
 // Dense-range variant used by tiles: every pair (i, j) with r0 <= i < r1, c0 <= j < c1, i < j.
 __global__ void synth_tile_kernel(int64_t n, int32_t r0, int32_t r1, int32_t c0, int32_t c1, uint64_t seed,
-                                  double* __restrict__ out, uint8_t* __restrict__ flags, double threshold) {
+                                  double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
+                                  const LedgerRef ledger) {
   const int64_t w = c1 - c0;
   const int64_t total = (int64_t)(r1 - r0) * w;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -50,6 +52,7 @@ __global__ void synth_tile_kernel(int64_t n, int32_t r0, int32_t r1, int32_t c0,
     const double v = __ull2double_rn(h) * 0x1p-64;
     const int64_t pid = pair_id(n, i, j);
     out[pid] = v;
+    ledger_mark(ledger, pid);
     if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
   }
 }
@@ -79,7 +82,7 @@ __global__ void synth_prnu_kernel(int64_t hw, int32_t first_key, int32_t n_items
 }  // namespace
 
 rk_status synth_compare(rk_app* app, const PairBatch& b, double* d_out, uint8_t* d_flags, cudaStream_t s) {
-  synth_compare_kernel<<<(b.npairs + 63) / 64, 64, 0, s>>>(b, app->p.seed, d_out, d_flags, threshold_or_nan(app));
+  synth_compare_kernel<<<(b.npairs + 63) / 64, 64, 0, s>>>(b, app->p.seed, d_out, d_flags, threshold_or_nan(app), app->ledger);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;
@@ -92,7 +95,7 @@ rk_status synth_tile(rk_app* app, int32_t r0, int32_t r1, int32_t c0, int32_t c1
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   synth_tile_kernel<<<blocks, 256, 0, s>>>(app->p.n, r0, r1, c0, c1, app->p.seed, d_out, d_flags,
-                                           threshold_or_nan(app));
+                                           threshold_or_nan(app), app->ledger);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;

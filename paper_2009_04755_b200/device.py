@@ -69,6 +69,20 @@ class DeviceApp:
         check(lib.rk_compare_pairs(self.handle, _ptr(slots), self.slot_stride, arr, len(plist), _ptr(out),
                                    _ptr(flags), _stream(stream)))
 
+    def set_ledger(self, region: Optional[torch.Tensor]) -> None:
+        """Mark every pair this app compares in `region` (rk_ledger_bytes(n) zeroed
+        device bytes, see ledger_region()); None turns the ledger off."""
+        check(lib.rk_app_set_ledger(self.handle, _ptr(region)))
+
+    def ledger_region(self) -> torch.Tensor:
+        nbytes = int(lib.rk_ledger_bytes(self.params.n))
+        return torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def ledger(self, region: torch.Tensor) -> dict:
+        st = _lib.LedgerStats()
+        check(lib.rk_ledger_read(_ptr(region), self.params.n, C.byref(st)))
+        return st.as_dict()
+
     def compare_tile(self, slots: Optional[torch.Tensor], r0: int, r1: int, c0: int, c1: int,
                      slot_of_key: Sequence[int], out: torch.Tensor, flags: Optional[torch.Tensor] = None,
                      stream=None) -> None:
@@ -140,6 +154,38 @@ class DeviceEngine:
     def reset_stats(self) -> None:
         check(lib.rk_engine_reset_stats(self.handle))
 
+    def ledger(self) -> dict:
+        """The exactly-once ledger this engine marks into (the job's shared one on
+        rank 0 after connect_peers): total, completed, dup_marks, full."""
+        st = _lib.LedgerStats()
+        check(lib.rk_engine_ledger(self.handle, C.byref(st)))
+        return st.as_dict()
+
+    def check_ledger(self) -> dict:
+        """Raise AssertionError (PairLedger.mark, scheduler.py:233-241) if any pair
+        completed twice; returns the ledger otherwise."""
+        led = self.ledger()
+        if led["dup_marks"]:
+            i, j = C.c_int64(), C.c_int64()
+            check(lib.rk_pair_from_id(self.params.n, led["first_dup_pid"], C.byref(i), C.byref(j)))
+            raise AssertionError(f"pair ({i.value}, {j.value}) completed twice ({led['dup_marks']} duplicate marks)")
+        return led
+
+    def use_ledger(self, region_ptr: int) -> None:
+        """Mark into the ledger region at a device address (e.g. another engine's)."""
+        check(lib.rk_engine_use_ledger(self.handle, region_ptr))
+
+    def ledger_region_ptr(self) -> int:
+        arena, stride = C.c_void_p(), C.c_size_t()
+        check(lib.rk_engine_arena(self.handle, C.byref(arena), C.byref(stride)))
+        off, nbytes = C.c_size_t(), C.c_size_t()
+        check(lib.rk_engine_ledger_region(self.handle, C.byref(off), C.byref(nbytes)))
+        return int(arena.value) + int(off.value)
+
+    def ledger_reset(self) -> None:
+        """Clear the shared ledger (rank 0; a no-op elsewhere) before the pre-run barrier."""
+        check(lib.rk_engine_ledger_reset(self.handle))
+
     def set_profiling(self, every: int, max_samples: int = 1024) -> None:
         check(lib.rk_engine_set_profiling(self.handle, every, max_samples))
 
@@ -206,16 +252,19 @@ class DeviceEngine:
         check(lib.rk_engine_arena(self.handle, C.byref(arena), C.byref(stride)))
         qword = C.c_void_p()
         check(lib.rk_engine_queue_word(self.handle, C.byref(qword)))
+        loff, lbytes = C.c_size_t(), C.c_size_t()
+        check(lib.rk_engine_ledger_region(self.handle, C.byref(loff), C.byref(lbytes)))
         hbuf = (C.c_uint8 * 64)()
         check(lib.rk_ipc_handle(arena, hbuf))
         a0 = int(arena.value)
-        mine = (bytes(hbuf), int(base.value or a0) - a0, int(qword.value) - a0)
+        mine = (bytes(hbuf), int(base.value or a0) - a0, int(qword.value) - a0, int(loff.value))
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
         homes = (C.c_void_p * self.world)()
         queues = (C.c_void_p * self.world)()
         self._opened = []
-        for r, (h, hoff, qoff) in enumerate(everyone):
+        ledger0 = None
+        for r, (h, hoff, qoff, lo) in enumerate(everyone):
             if r == self.rank:
                 pbase = a0
             else:
@@ -225,6 +274,10 @@ class DeviceEngine:
                 pbase = int(peer.value)
             homes[r] = pbase + hoff
             queues[r] = pbase + qoff
+            if r == 0:
+                ledger0 = pbase + lo
+        # one exactly-once ledger for the whole job: rank 0's, marked over NVLink
+        check(lib.rk_engine_use_ledger(self.handle, ledger0))
         if self.peer_tier:
             check(lib.rk_engine_set_peer_homes(self.handle, self.world, homes))
         if self.steal:

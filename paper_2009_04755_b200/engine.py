@@ -42,6 +42,7 @@ class RunResult:
     seconds: float = 0.0
     trace: list = field(default_factory=list)      # metrics.py TraceEvent dicts (when tracing)
     node: dict = field(default_factory=dict)       # this rank's NodeMetrics dict
+    ledger: dict = field(default_factory=dict)     # exactly-once ledger of the job (rank 0): completed, full
 
     @property
     def pairs(self) -> int:
@@ -147,7 +148,9 @@ class AllPairsEngine:
         self._eng.reset_stats()
         t0 = time.perf_counter()
         stride = self.app.parsed_bytes()
-        shared = self._eng.peer_tier or self._eng.steal
+        # world > 1: the ranks share rank 0's exactly-once ledger over IPC (and, with the
+        # peer tier / stealing, each other's home regions and queue words)
+        shared = self.world > 1
         if self._eng.peer_tier:
             # home items first (k % world == rank), then the IPC-mapped peer homes
             # home item m = key rank + m*world: a strided view of the full item array
@@ -170,11 +173,13 @@ class AllPairsEngine:
                 self._peers_connected = True
             if self._eng.steal:
                 self._eng.queue_reset()
-            dist.barrier()   # home regions complete and queue words reset before anyone reads them
+            self._eng.ledger_reset()   # rank 0 clears the job's ledger
+            dist.barrier()   # home regions complete, queue words and ledger reset before anyone uses them
         self._eng.run(self._out, self._flags, host_items=host_items, device_items=device_items,
                       parsed_stride=stride)
         if shared:
-            dist.barrier()   # peers are done reading our home region and queue word
+            dist.barrier()   # peers are done reading our home region and queue word, all marks landed
+        ledger = self._eng.check_ledger() if self.rank == 0 else {}   # AssertionError on a duplicate
         if self.world > 1 and gather:
             gather_triangle(self._out, self._flags)
         values = self._out.cpu().numpy()
@@ -184,7 +189,7 @@ class AllPairsEngine:
         events = self._eng.trace(node=self.rank) if self._trace_on else []
         from .metrics import node_metrics
         return RunResult(self.app.n, values, flags, stats, seconds, events,
-                         node_metrics(self.rank, stats, seconds, self._slots, events))
+                         node_metrics(self.rank, stats, seconds, self._slots, events), ledger)
 
     def metrics(self, result: RunResult, config: Optional[dict] = None,
                 costs: Optional[perfmodel.StageCosts] = None) -> dict:

@@ -52,11 +52,13 @@ def main():
     ce.load_home(device_items=_At(rank * stride), parsed_stride=world * stride)
     ce.connect_peers()
     ce.queue_reset()
+    ce.ledger_reset()
     dist.barrier()
     cv_out = torch.zeros(m * (m - 1) // 2, dtype=torch.float64, device="cuda")
     cv_flags = torch.zeros_like(cv_out, dtype=torch.uint8)
     ce.run(cv_out, cv_flags, device_items=buf, parsed_stride=stride)
     dist.barrier()
+    cv_ledger = ce.check_ledger() if rank == 0 else None
     gather_triangle(cv_out, cv_flags)
     ce.close()
 
@@ -80,6 +82,7 @@ def main():
             "pce_flags_once": bool(np.all((res.flags == 1) | (res.flags == 3))),
             "cv_bit_exact_vs_1gpu": bool(torch.equal(cv_out, cv_solo)),
             "cv_flags_once": bool(((cv_flags == 1) | (cv_flags == 3)).all().item()),
+            "pce_ledger_full": bool(res.ledger["full"]), "cv_ledger_full": bool(cv_ledger["full"]),
         })
         print("MGPU_REPORT " + json.dumps(report), flush=True)
     dist.barrier()

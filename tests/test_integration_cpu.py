@@ -1,6 +1,7 @@
 """The reference-side binding (integration/allpairs_b200.py) against the reference's
-own Application contract.  Runs only where the reference package is importable
-(this container); the GPU box has no /root/reference and skips it."""
+own Application contract.  Uses the reference package staged in oracle/_ref
+(oracle/Makefile) or /root/reference; runs the compare path in
+tests/test_dropin_gpu.py."""
 
 import ctypes as C
 import importlib.util
@@ -9,12 +10,13 @@ import sys
 
 import pytest
 
-REF = "/root/reference/pkg/src"
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = next((p for p in (os.path.join(HERE, "oracle", "_ref"), "/root/reference/pkg/src")
+            if os.path.isdir(os.path.join(p, "allpairs"))), None)
 
 
 def _binding():
-    if not os.path.isdir(REF):
+    if REF is None:
         pytest.skip("reference package not present")
     sys.dont_write_bytecode = True      # never write into the (read-only) reference tree
     sys.path.insert(0, REF)
@@ -29,9 +31,16 @@ def test_binding_is_a_reference_application_with_matching_abi():
     mod = _binding()
     from allpairs.apps import Application
     from paper_2009_04755_b200 import _lib
+    from allpairs.apps import CompositionVectorApp
     assert issubclass(mod.B200PCEApp, Application)
     for name in ("preprocess", "compare", "postprocess", "stage_cost"):
         assert getattr(mod.B200PCEApp, name) is not getattr(Application, name)
+    # the CV drop-in keeps the reference's corpus I/O and parse, replaces preprocess/compare
+    assert issubclass(mod.B200CompositionVectorApp, CompositionVectorApp)
+    for name in ("path_for_key", "fetch_raw", "parse", "postprocess"):
+        assert getattr(mod.B200CompositionVectorApp, name) is getattr(CompositionVectorApp, name)
+    for name in ("preprocess", "compare"):
+        assert getattr(mod.B200CompositionVectorApp, name) is not getattr(CompositionVectorApp, name)
     # the binding's structs are the header's (same layout as the package's own ctypes mirror)
     assert C.sizeof(mod.RkAppParams) == C.sizeof(_lib.AppParams)
     assert [f[0] for f in mod.RkAppParams._fields_] == [f[0] for f in _lib.AppParams._fields_]

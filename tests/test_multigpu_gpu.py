@@ -37,3 +37,4 @@ def test_multi_gpu_bit_exact_vs_single_gpu():
     assert r["pce_bit_exact_vs_1gpu"] and r["pce_flags_once"]
     assert r["cv_bit_exact_vs_1gpu"] and r["cv_flags_once"]
     assert r["peer_fetches"] > 0
+    assert r["pce_ledger_full"] and r["cv_ledger_full"]          # the shared device ledger on rank 0

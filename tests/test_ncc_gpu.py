@@ -62,7 +62,7 @@ def test_gram_sharded_across_ranks_covers_all_pairs():
         acc += out
         done += eng.stats()["pairs_done"]
     assert done == total
-    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    want = oncc.all_pairs_chunked(items.cpu().numpy().reshape(n, side, side))
     assert np.max(np.abs(acc.cpu().numpy() - want)) <= 2e-4
 
 
@@ -127,12 +127,14 @@ def test_gram_blocks_over_a_partial_arena():
         device.ncc_gram_block(app, slots, arena_rows, 0, 0, 256, 384, 128, 256, out)
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_engine_blocked_gram_when_items_exceed_slots(world):
+@pytest.mark.parametrize("world,side", [(1, 128), (2, 128), (1, 512)])
+def test_engine_blocked_gram_when_items_exceed_slots(world, side):
     """device_slots < n: the engine runs the Gram over key blocks that fit (half the
-    arena each), loading blocks as needed; ranks take block pairs round-robin."""
+    arena each), loading blocks as needed; ranks take block pairs round-robin.
+    side 512: D = 262,144 = two K chunks, so every block triangle and rectangle
+    also goes through the chunk-accumulate epilogue."""
     _l, device = _mods()
-    n, side = 600, 128
+    n = 600
     items = make_items(n, side, seed=14)
     total = n * (n - 1) // 2
     acc = torch.zeros(total, dtype=torch.float64, device="cuda")
@@ -152,5 +154,33 @@ def test_engine_blocked_gram_when_items_exceed_slots(world):
     assert done == total and loads > n            # blocks reloaded: R > 1
     f = fl.cpu().numpy()
     assert np.all((f == 1) | (f == 3))             # every pair exactly once
-    want = oncc.all_pairs(items.cpu().numpy().reshape(n, side, side).astype(np.float64))
+    want = oncc.all_pairs_chunked(items.cpu().numpy().reshape(n, side, side))
     assert np.max(np.abs(acc.cpu().numpy() - want)) <= 2e-4
+
+
+@pytest.mark.parametrize("side", [512, 1024])
+def test_gram_multi_k_chunk_matches_oracle(side):
+    """BASELINE item sizes take the K-chunked Gram: D = side^2 is streamed in chunks
+    of 131,072 elements, one launch each; chunk 0 stores, later chunks add into
+    out[pid] in fp64 and the last one writes the flags (ncc.cu).  512^2 = 2 chunks,
+    1024^2 = 8 chunks (the C2/C3 item size class).  n = 300 runs the CTA-pair
+    256 x 256 kernel with a ragged last tile.  Bound: |error| <= 2e-4 (TF32)."""
+    _l, device = _mods()
+    n = 300
+    items = make_items(n, side, seed=19, cameras=6)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_NCC, n, height=side, width=side, threshold=0.02),
+                              device_slots=n)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    want = oncc.all_pairs_chunked(items.cpu().numpy().reshape(n, side * side))
+    assert np.all(np.isfinite(got))
+    err = np.max(np.abs(got - want))
+    assert err <= 2e-4, err
+    f = flags.cpu().numpy()
+    assert np.all((f == 1) | (f == 3)) and np.array_equal(f == 3, got >= 0.02)
+    st = eng.stats()
+    assert st["pairs_done"] == total and st["loads"] == n

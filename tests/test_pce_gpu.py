@@ -249,3 +249,67 @@ def test_engine_tight_tier_completes():
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=RTOL)
     st = eng.stats()
     assert st["pairs_done"] == total and st["pinned_at_end"] == 0 and st["evictions"] > 0
+
+
+@pytest.mark.parametrize("side,n,cams", [(1024, 64, 8), (256, 72, 6)])
+def test_engine_bench_path_many_pairs_per_cta(side, n, cams):
+    """The exact path bench.py times, checked pair by pair against the oracle.
+
+    Engine, leaf 8, all items resident, device inputs -- as bench.py -- with n
+    large enough that a compare launch carries a whole number of rounds of the
+    persistent grid (1,924 pairs = 13 per CTA at 1024^2 on 148 SMs).  Every CTA
+    therefore runs several pairs back to back: carried mbarrier phases, T-slot
+    reuse and the staging-buffer refills are all on this path.  Every pair of the
+    job is compared with the float64 oracle (scipy-batched inverse FFTs)."""
+    _l, device = _lib()
+    items = make_items(n, side, cameras=cams, seed=17)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side, threshold=60.0),
+                              leaf_block=8, device_slots=n)
+    eng.set_profiling(every=1, max_samples=256)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+    _, launches, launched_pairs = eng.kernel_time()
+    assert launched_pairs == total
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    # pairs per launch exceed the number of persistent CTAs several times over
+    assert total / launches >= 4 * sms, (total, launches, sms)
+    host = items.cpu().numpy().reshape(n, side, side)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    want = opce.pairs_batched(host, pairs)
+    got = out.cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=RTOL)
+    f = flags.cpu().numpy()
+    assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))
+    st = eng.stats()
+    assert st["pairs_done"] == total and st["loads"] == n
+
+
+def test_2048_many_pairs_per_cta_sampled():
+    """C3 item shape, 780 pairs in one launch (> 5 per persistent CTA), through the
+    engine as bench.py --side 2048 (and its C3 mode) runs it; 96 sampled pairs
+    (first and last pairs of the launch included) against the float64 oracle."""
+    _l, device = _lib()
+    side, n = 2048, 40
+    items = make_items(n, side, cameras=4, seed=23)
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side, threshold=60.0),
+                              leaf_block=8, device_slots=n)
+    eng.set_profiling(every=1, max_samples=64)
+    total = n * (n - 1) // 2
+    out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+    flags = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    eng.run(out, flags, device_items=items, parsed_stride=side * side * 4)
+    _, launches, launched_pairs = eng.kernel_time()
+    assert launched_pairs == total and launches == 1
+    got = out.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    rng = np.random.default_rng(5)
+    pids = sorted(set([0, 1, total - 2, total - 1] + rng.choice(total, 92, replace=False).tolist()))
+    from oracle import scheduler as osch
+    pairs = [osch.pair_from_id(n, int(p)) for p in pids]
+    host = items.cpu().numpy().reshape(n, side, side)
+    want = opce.pairs_batched(host, pairs, batch=4)
+    np.testing.assert_allclose(got[pids], want, rtol=RTOL)
+    f = flags.cpu().numpy()
+    assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))

@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0):
+def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0, n=26):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -27,7 +27,7 @@ def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0):
     try:
         from paper_2009_04755_b200.apps import PCEApp
         from paper_2009_04755_b200.engine import AllPairsEngine
-        app = PCEApp(26, side=256, cameras=3, seed=17, device=0)
+        app = PCEApp(n, side=256, cameras=3, seed=17, device=0)
         eng = AllPairsEngine(app, leaf_block=4, device_slots=10, rank=rank, world=world, peer_tier=True,
                              steal_chunk=steal_chunk)
         if rank == 0 and delay0 > 0:
@@ -40,7 +40,7 @@ def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0):
                 return inner(*a, **kw)
             eng._eng.run = late_run
         res = eng.run(gather=False)
-        ret.put((rank, res.values.copy(), res.flags.copy(), res.stats))
+        ret.put((rank, res.values.copy(), res.flags.copy(), dict(res.stats, ledger=res.ledger)))
         eng.close()
     finally:
         dist.destroy_process_group()
@@ -74,36 +74,44 @@ def test_two_ranks_peer_fetch_match_oracle(steal_chunk, delay0):
         assert st["loads"] == 13                                 # only home items preprocessed: R = 1
         assert st["peer_fetches"] > 0 and st["peer_bytes"] == st["peer_fetches"] * 256 * 256 * 4
     assert outs[0][3]["pairs_done"] + outs[1][3]["pairs_done"] == 26 * 25 // 2
+    led = outs[0][3]["ledger"]                                   # the job's shared ledger, on rank 0
+    assert led["full"] == 1 and led["completed"] == 26 * 25 // 2 and led["dup_marks"] == 0
     if delay0 > 0:
         assert outs[1][3]["steals"] >= 1                         # the idle rank stole from the late one
         assert outs[1][3]["pairs_done"] > outs[0][3]["pairs_done"]
 
 
-def test_three_ranks_steal_from_a_late_rank():
-    """Three ranks (IPC-shared cuda:0): rank 0 starts 3 s late, the other two drain
+@pytest.mark.parametrize("world,n", [(3, 26), (8, 48)])
+def test_ranks_steal_from_a_late_rank(world, n):
+    """`world` ranks (IPC-shared cuda:0): rank 0 starts 3 s late, the others drain
     their shares and then steal from it -- and from each other's stolen ranges --
-    while every pair is still computed exactly once and matches the oracle."""
+    while every pair is still computed exactly once (the shared device ledger on
+    rank 0 and the summed flags agree) and matches the oracle.  world = 8 runs the
+    8-GPU box's queue scan, 8 IPC mappings and the shared ledger on one GPU."""
     import torch.multiprocessing as mp
     from oracle import pce as opce
     from paper_2009_04755_b200.apps import PCEApp
-    world = 3
     ctx = mp.get_context("spawn")
     ret = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, ret, 1, 3.0)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, ret, 1, 3.0, n)) for r in range(world)]
     for p in procs:
         p.start()
-    outs = sorted([ret.get(timeout=300) for _ in range(world)], key=lambda o: o[0])
+    outs = sorted([ret.get(timeout=600) for _ in range(world)], key=lambda o: o[0])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    total = n * (n - 1) // 2
     values = sum(o[1] for o in outs)
     flags = sum(o[2].astype(np.int32) for o in outs)
-    app = PCEApp(26, side=256, cameras=3, seed=17)
+    app = PCEApp(n, side=256, cameras=3, seed=17)
     pats = np.stack([np.frombuffer(app.fetch_raw(app.path_for_key(k)), dtype=np.float32).reshape(256, 256)
-                     for k in range(26)])
+                     for k in range(n)])
     np.testing.assert_allclose(values, opce.all_pairs(pats), rtol=1e-4)
     assert set(np.unique(flags)) <= {1, 3}
-    assert sum(o[3]["pairs_done"] for o in outs) == 26 * 25 // 2
-    assert outs[1][3]["steals"] + outs[2][3]["steals"] >= 1
-    assert outs[0][3]["pairs_done"] < min(outs[1][3]["pairs_done"], outs[2][3]["pairs_done"])
+    assert sum(o[3]["pairs_done"] for o in outs) == total
+    assert sum(o[3]["steals"] for o in outs[1:]) >= 1
+    assert outs[0][3]["pairs_done"] < min(o[3]["pairs_done"] for o in outs[1:])
+    assert sum(o[3]["loads"] for o in outs) == n                 # every item preprocessed once, on its home rank
+    led = outs[0][3]["ledger"]
+    assert led["full"] == 1 and led["completed"] == total and led["dup_marks"] == 0
