@@ -163,6 +163,9 @@ typedef struct {
   int32_t peer_tier;       /* world > 1: items live on their home GPU (k mod world), others fetch them over NVLink */
   int32_t steal;           /* world > 1: dynamic leaf chunks + cross-GPU stealing through device atomics */
   int32_t steal_chunk;     /* leaves per grab (0: one compare batch worth) */
+  int32_t host_slots;      /* host (L2) tier of preprocessed items in pinned memory, write-through
+                              (engine.py:375-394, :482-508); 0 = none.  Single-GPU runs only: with the
+                              peer tier the home GPU is the next level (distcache.py owner_of) */
 } rk_engine_params;
 
 typedef struct {
@@ -182,6 +185,9 @@ typedef struct {
   int64_t writing_at_end;  /* device slots still in WRITE when the run returned (must be 0) */
   int64_t ledger_marked;   /* pair ids set in the engine's own ledger after the run (-1: ledger shared, see rk_engine_ledger) */
   int64_t dup_marks;       /* duplicate completions seen by the engine's own ledger */
+  int64_t host_hits;       /* host tier (slotcache.py:166-170): device misses served from pinned host slots */
+  int64_t host_misses;     /* host tier misses (fresh loads, written through to the host tier) */
+  int64_t host_evictions;
 } rk_engine_stats;
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params,

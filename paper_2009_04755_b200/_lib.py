@@ -62,6 +62,7 @@ class EngineParams(C.Structure):
         ("peer_tier", C.c_int32),
         ("steal", C.c_int32),
         ("steal_chunk", C.c_int32),
+        ("host_slots", C.c_int32),
     ]
 
 
@@ -83,6 +84,9 @@ class EngineStats(C.Structure):
         ("writing_at_end", C.c_int64),
         ("ledger_marked", C.c_int64),
         ("dup_marks", C.c_int64),
+        ("host_hits", C.c_int64),
+        ("host_misses", C.c_int64),
+        ("host_evictions", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

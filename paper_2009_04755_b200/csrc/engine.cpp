@@ -313,6 +313,11 @@ struct rk_engine {
   void* staging = nullptr;
   int staging_items = 0;
   rk::SlotTier* tier = nullptr;
+  // host (L2) tier of preprocessed items: the reference's host CacheTier
+  // (slotcache.py:139-282) over pinned host slots, written through on every fresh
+  // load (engine.py:482-508) and read back H2D on a device miss (engine.py:375-394)
+  rk::SlotTier* htier = nullptr;
+  char* harena = nullptr;
   rk_engine_stats stats{};
   // peer-GPU tier (distcache.py owner_of: home(k) = k mod world): this rank's home
   // items live at arena slots [arena_slots, arena_slots + home_slots), item k at
@@ -351,6 +356,7 @@ namespace {
 struct LoadReq {
   int32_t key;
   int32_t slot;
+  int32_t hslot = -1;   // host-tier slot: write-through target (fresh load) or source (host hit)
 };
 
 // Device timestamps of the finished run's trace records, relative to its start.
@@ -451,8 +457,41 @@ rk_status flush_loads(rk_engine* e, std::vector<LoadReq>& loads, const void* h_p
     trace_end(e, tk, e->lstream);
     e->stats.loads += m;
   }
-  for (const LoadReq& l : loads) e->tier->publish(l.slot, true);  // retained lease (slotcache.py:188-213)
+  for (const LoadReq& l : loads) {
+    e->tier->publish(l.slot, true);  // retained lease (slotcache.py:188-213)
+    if (l.hslot >= 0) {
+      // write-through: the host copy is published with (here: right after) the device
+      // copy (engine.py:482-487, assert :503); stream order on the load stream keeps a
+      // later reuse of this host slot behind the copy
+      RK_CUDA(cudaMemcpyAsync(e->harena + (size_t)l.hslot * e->slot_stride,
+                              static_cast<char*>(e->arena) + (size_t)l.slot * e->slot_stride, e->app->slot_bytes,
+                              cudaMemcpyDeviceToHost, e->lstream));
+      e->stats.d2h_bytes += (int64_t)e->app->slot_bytes;
+      e->htier->publish(l.hslot, false);
+    }
+  }
   loads.clear();
+  RK_CUDA(cudaEventRecord(e->ev_loaded, e->lstream));
+  e->loads_unsynced = true;
+  return RK_OK;
+}
+
+// Device misses served by the host tier: H2D of the preprocessed slot, no parse /
+// preprocess (not a load, engine.py:443-448); the host lease ends once the copy
+// is enqueued (later host-slot reuse is ordered behind it on the load stream).
+rk_status flush_host_hits(rk_engine* e, std::vector<LoadReq>& hits) {
+  if (hits.empty()) return RK_OK;
+  const int tk = trace_begin(e, 1, hits[0].key, -1, (int)hits.size(), e->lstream);
+  for (const LoadReq& h : hits) {
+    RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + (size_t)h.slot * e->slot_stride,
+                            e->harena + (size_t)h.hslot * e->slot_stride, e->app->slot_bytes, cudaMemcpyHostToDevice,
+                            e->lstream));
+    e->stats.h2d_bytes += (int64_t)e->app->slot_bytes;
+    e->htier->release(h.hslot);
+    e->tier->publish(h.slot, true);
+  }
+  trace_end(e, tk, e->lstream);
+  hits.clear();
   RK_CUDA(cudaEventRecord(e->ev_loaded, e->lstream));
   e->loads_unsynced = true;
   return RK_OK;
@@ -585,6 +624,14 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   ce = cudaMalloc(&e->staging, std::max<size_t>(e->app->parsed_bytes, 16) * e->staging_items);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaMalloc(staging)"));
   e->tier = new SlotTier(params->device_slots);
+  if (params->host_slots > 0 && !(params->peer_tier && params->world > 1) && app_params->kind != RK_APP_NCC &&
+      app_params->kind != RK_APP_SYNTHETIC) {
+    if (params->host_slots < 2) return fail(set_error(RK_ERR_VALUE, "host tiers need >= 2 slots"));
+    e->htier = new SlotTier(params->host_slots);
+    ce = cudaHostAlloc(reinterpret_cast<void**>(&e->harena), (size_t)params->host_slots * e->slot_stride,
+                       cudaHostAllocDefault);
+    if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaHostAlloc(host tier)"));
+  }
   *out = e;
   return RK_OK;
 }
@@ -605,6 +652,8 @@ void rk_engine_destroy(rk_engine* e) {
   if (e->h_qres) cudaFreeHost(e->h_qres);
   cudaFree(e->arena);
   cudaFree(e->staging);
+  if (e->harena) cudaFreeHost(e->harena);
+  delete e->htier;
   delete e->tier;
   rk_app_destroy(e->app);
   delete e;
@@ -663,6 +712,13 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
     e->tier->hits = h;
     e->tier->misses = m;
     e->tier->evictions = ev;
+    if (e->htier) {
+      const int64_t hh = e->htier->hits, hm = e->htier->misses, he = e->htier->evictions;
+      *e->htier = SlotTier(e->htier->capacity);
+      e->htier->hits = hh;
+      e->htier->misses = hm;
+      e->htier->evictions = he;
+    }
   }
   const int64_t launches0 = e->app->launches;
   e->tr.clear();
@@ -718,6 +774,7 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
   std::vector<rk_pair> pend;
   std::vector<LoadReq> loads;
   std::vector<LoadReq> fetches;
+  std::vector<LoadReq> host_hits;
   std::vector<int32_t> keys;
   std::vector<int32_t> pinned;
   std::vector<int32_t> slot_of(peer ? n : 0, -1);
@@ -761,8 +818,16 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
       TierResult r = e->tier->acquire(k);
       if (r.kind == kNoEvictable) {
         for (int s : pinned) e->tier->release(s);
-        for (const LoadReq& q : loads) e->tier->abort(q.slot);
+        for (const LoadReq& q : loads) {
+          e->tier->abort(q.slot);
+          if (q.hslot >= 0) e->htier->abort(q.hslot);
+        }
+        for (const LoadReq& q : host_hits) {
+          e->tier->abort(q.slot);
+          e->htier->release(q.hslot);
+        }
         loads.clear();
+        host_hits.clear();
         return set_error(RK_ERR_NO_EVICTABLE, "all %d device slots are pinned (leaf needs %zu)", e->tier->capacity,
                          keys.size());
       }
@@ -774,12 +839,22 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
           RK_CUDA(cudaEventRecord(e->ev_compared, e->stream));
           RK_CUDA(cudaStreamWaitEvent(e->lstream, e->ev_compared, 0));
         }
-        if (peer) fetches.push_back(LoadReq{k, r.slot});
-        else loads.push_back(LoadReq{k, r.slot});
+        if (peer) {
+          fetches.push_back(LoadReq{k, r.slot});
+        } else if (e->htier) {
+          // next level down: the host tier (engine.py:375-394)
+          const TierResult hr = e->htier->acquire(k);
+          if (hr.kind == kHit || hr.kind == kMustWait) host_hits.push_back(LoadReq{k, r.slot, hr.slot});
+          else if (hr.kind == kMiss) loads.push_back(LoadReq{k, r.slot, hr.slot});
+          else loads.push_back(LoadReq{k, r.slot});   // every host slot pinned: load without write-through
+        } else {
+          loads.push_back(LoadReq{k, r.slot});
+        }
       }
       pinned.push_back(r.slot);
       if (peer) slot_of[k] = r.slot;
     }
+    RK_TRY(flush_host_hits(e, host_hits));
     RK_TRY(flush_loads(e, loads, h_parsed, d_parsed, parsed_stride));
     if (!fetches.empty()) {
       // peer tier hit: copy the preprocessed item from its home GPU over NVLink
@@ -868,6 +943,11 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
   e->stats.hits = e->tier->hits;
   e->stats.misses = e->tier->misses;
   e->stats.evictions = e->tier->evictions;
+  if (e->htier) {
+    e->stats.host_hits = e->htier->hits;
+    e->stats.host_misses = e->htier->misses;
+    e->stats.host_evictions = e->htier->evictions;
+  }
   e->stats.kernel_launches += e->app->launches - launches0;
   return RK_OK;
 }
@@ -928,6 +1008,7 @@ rk_status rk_engine_reset_stats(rk_engine* e) {
   e->stats = rk_engine_stats{};
   e->steals = 0;
   e->tier->hits = e->tier->misses = e->tier->waits = e->tier->evictions = 0;
+  if (e->htier) e->htier->hits = e->htier->misses = e->htier->waits = e->htier->evictions = 0;
   return RK_OK;
 }
 

@@ -113,13 +113,13 @@ class DeviceEngine:
 
     def __init__(self, params: _lib.AppParams, *, leaf_block: int = 8, device_slots: int = 0,
                  rank: int = 0, world: int = 1, device: int = 0, peer_tier: bool = False, steal: bool = False,
-                 steal_chunk: int = 0):
+                 steal_chunk: int = 0, host_slots: int = 0):
         self.params = params
         self.device = device
         self.rank, self.world = rank, world
         slots = device_slots if device_slots > 0 else max(2, params.n)
         ep = _lib.EngineParams(leaf_block, slots, 1, rank, world, int(bool(peer_tier and world > 1)),
-                               int(bool(steal and world > 1)), steal_chunk)
+                               int(bool(steal and world > 1)), steal_chunk, host_slots)
         handle = C.c_void_p()
         check(lib.rk_engine_create(C.byref(params), C.byref(ep), device, C.byref(handle)))
         self.handle = handle

@@ -107,7 +107,7 @@ class AllPairsEngine:
 
     def __init__(self, app: B200Application, *, leaf_block: int = 16, device_slots: Optional[int] = None,
                  rank: int = 0, world: int = 1, peer_tier: bool = True, steal: bool = True,
-                 steal_chunk: int = 0, trace_events: int = 0):
+                 steal_chunk: int = 0, trace_events: int = 0, host_slots: int = 0):
         self.app = app
         self.rank = rank
         self.world = world
@@ -116,7 +116,8 @@ class AllPairsEngine:
         self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
                                  rank=rank, world=world, device=app.device,
                                  peer_tier=peer_tier and world > 1 and app.kind not in (0, 3),
-                                 steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk)
+                                 steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk,
+                                 host_slots=host_slots)
         self._peers_connected = False
         self._slots = max(2, slots)
         if trace_events:

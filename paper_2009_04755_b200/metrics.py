@@ -50,8 +50,11 @@ def node_metrics(node: int, stats: dict, seconds: float, device_slots: int, even
         "steals_remote": stats.get("steals", 0),
         "steal_requests_failed": 0,
         "messages_sent": {},
-        "cache": {"dev0": {"hits": stats.get("hits", 0), "misses": stats.get("misses", 0), "waits": 0,
-                           "evictions": stats.get("evictions", 0), "occupancy": device_slots}},
+        "cache": dict({"dev0": {"hits": stats.get("hits", 0), "misses": stats.get("misses", 0), "waits": 0,
+                                "evictions": stats.get("evictions", 0), "occupancy": device_slots}},
+                      **({"host": {"hits": stats["host_hits"], "misses": stats["host_misses"], "waits": 0,
+                                   "evictions": stats["host_evictions"], "occupancy": stats["host_misses"]}}
+                         if stats.get("host_hits", 0) + stats.get("host_misses", 0) else {})),
         "remote_requests": stats.get("peer_fetches", 0),
         "remote_hits_by_hop": {"1": stats.get("peer_fetches", 0)} if stats.get("peer_fetches", 0) else {},
         "remote_failures": 0,

@@ -16,6 +16,16 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-4
 
 
+def assert_pce_parity(got, cands, rtol=RTOL):
+    """Every device value equals the oracle's PCE at its argmax -- or, where the
+    float64 plane has another location within 1e-5 of the peak, the PCE at that
+    near-tie (oracle/pce.py pce_candidates).  Near-ties are rare and counted."""
+    bad = [k for k, c in enumerate(cands) if not opce.matches(float(got[k]), c, rtol)]
+    assert not bad, [(k, float(got[k]), cands[k].tolist()) for k in bad[:8]]
+    ties = sum(1 for k, c in enumerate(cands) if not opce.matches(float(got[k]), c[:1], rtol))
+    return ties
+
+
 def _lib():
     from paper_2009_04755_b200 import _lib, device
     return _lib, device
@@ -277,9 +287,10 @@ def test_engine_bench_path_many_pairs_per_cta(side, n, cams):
     assert total / launches >= 4 * sms, (total, launches, sms)
     host = items.cpu().numpy().reshape(n, side, side)
     pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
-    want = opce.pairs_batched(host, pairs)
+    cands = opce.pairs_batched(host, pairs, candidates=True)
     got = out.cpu().numpy()
-    np.testing.assert_allclose(got, want, rtol=RTOL)
+    ties = assert_pce_parity(got, cands)
+    assert ties <= max(2, total // 500)      # near-ties are rare: not a systematic offset
     f = flags.cpu().numpy()
     assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))
     st = eng.stats()
@@ -309,7 +320,42 @@ def test_2048_many_pairs_per_cta_sampled():
     from oracle import scheduler as osch
     pairs = [osch.pair_from_id(n, int(p)) for p in pids]
     host = items.cpu().numpy().reshape(n, side, side)
-    want = opce.pairs_batched(host, pairs, batch=4)
-    np.testing.assert_allclose(got[pids], want, rtol=RTOL)
+    cands = opce.pairs_batched(host, pairs, batch=4, candidates=True)
+    assert_pce_parity(got[pids], cands)
     f = flags.cpu().numpy()
     assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))
+
+
+@pytest.mark.parametrize("host_slots", [0, 8, 24])
+def test_engine_host_tier_write_through(host_slots):
+    """Host (L2) tier of preprocessed items (engine.py:375-394, write-through
+    :482-508): with a device tier far smaller than n, device misses are served from
+    pinned host slots instead of re-preprocessing; with host_slots >= n every item
+    is preprocessed exactly once (R = 1), smaller host tiers evict (LRU) and reload.
+    Results are bit-identical to the run without a host tier."""
+    _l, device = _lib()
+    side, n = 256, 24
+    items = make_items(n, side, cameras=3, seed=31)
+    total = n * (n - 1) // 2
+    eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=4,
+                              device_slots=6, host_slots=host_slots)
+    out = torch.zeros(total, dtype=torch.float64, device="cuda")
+    host = items.cpu().pin_memory()
+    eng.run(out, host_items=host, parsed_stride=side * side * 4)
+    st = eng.stats()
+    got = out.cpu().numpy()
+    ref = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=4, device_slots=n)
+    want = torch.zeros(total, dtype=torch.float64, device="cuda")
+    ref.run(want, device_items=items, parsed_stride=side * side * 4)
+    np.testing.assert_array_equal(got, want.cpu().numpy())
+    assert st["evictions"] > 0 and st["pinned_at_end"] == 0 and st["ledger_marked"] == total
+    if host_slots == 0:
+        assert st["loads"] > n and st["host_hits"] == 0
+    else:
+        assert st["host_hits"] > 0 and st["host_hits"] + st["host_misses"] == st["misses"]
+        assert st["loads"] == st["host_misses"]                       # a load is a fresh preprocess
+        assert st["d2h_bytes"] == st["host_misses"] * side * side * 4  # written through once per load
+        if host_slots >= n:
+            assert st["loads"] == n and st["host_evictions"] == 0     # R = 1
+        else:
+            assert st["loads"] > n and st["host_evictions"] > 0
