@@ -73,13 +73,14 @@ def parse_args(argv=None):
     ap.add_argument("--trace-dir", default="",
                     help="pce: after the timed steps, run one traced step and write the reference-schema "
                          "trace (JSONL) and run-metrics document of each rank here")
-    ap.add_argument("--app", default="pce", choices=["pce", "gmm", "cv"],
-                    help="pce: configs[1] (default); gmm: configs[3]; cv: configs[4]")
+    ap.add_argument("--app", default="pce", choices=["pce", "ncc", "gmm", "cv"],
+                    help="pce: configs[1] (default); ncc: the zero-lag NCC Gram of the same items (C3-Gram with "
+                         "--items 16384 --side 2048); gmm: configs[3]; cv: configs[4]")
     ap.add_argument("--angles", type=int, default=36, help="gmm: rotation grid K")
     ap.add_argument("--mean-nnz", type=float, default=5e5, help="cv: mean tokens per item")
     args = ap.parse_args(argv)
     if args.items <= 0:
-        args.items = {"pce": 4096, "gmm": 1000, "cv": 2500}[args.app]
+        args.items = {"pce": 4096, "ncc": 4096, "gmm": 1000, "cv": 2500}[args.app]
     if args.cameras <= 0:
         args.cameras = 256 if args.items >= 16384 else 64
     return args
@@ -102,18 +103,21 @@ def workload(args, world):
     n = args.items
     pairs_total = n * (n - 1) // 2
     metric = "pairs/sec (whole box)"
-    if args.app == "pce":
+    if args.app in ("pce", "ncc"):
         side = args.side
         cfg_name = {(128, 256): " (BASELINE configs[0])", (4096, 1024): " (BASELINE configs[1])",
                     (16384, 2048): " (BASELINE configs[2])"}.get((n, side), "")
         name = f"PRNU PCE all-pairs, N={n} patterns of {side}x{side} fp32{cfg_name}"
+        if args.app == "ncc":
+            name = (f"zero-lag NCC all-pairs as a tcgen05 TF32 Gram, N={n} patterns of {side}x{side} fp32"
+                    f"{cfg_name.replace(')', ', C3-Gram of SURVEY 8(d))') if cfg_name else ''}")
         pat = n * side * side * 4
         cfg = {"workload": name, "n": n, "side": side, "pairs": pairs_total, "leaf_block": args.leaf,
                "cameras": args.cameras, "parallelism": f"pairs{world}",
                "l2": f"inputs ({2 * pat / 2**30:.1f} GiB patterns + spectra) >> L2 (126 MB): no flush needed"}
         if home_only(args):
             cfg["placement"] = "home-only: item k generated + preprocessed on GPU k mod N, peers fetch over NVLink"
-        return metric, cfg, "fp32"
+        return metric, cfg, "tf32" if args.app == "ncc" else "fp32"
     if args.app == "gmm":
         name = (f"particle fusion (GMM/Bhattacharyya), N={n} particles of ~300 localizations, "
                 f"K={args.angles} rotations (BASELINE configs[3])")
@@ -129,7 +133,7 @@ def workload(args, world):
 
 def home_only(args) -> bool:
     """C3-sized PCE jobs: patterns + spectra of all items do not fit one GPU."""
-    return args.app == "pce" and 2 * args.items * args.side * args.side * 4 > (120 << 30)
+    return args.app in ("pce", "ncc") and 2 * args.items * args.side * args.side * 4 > (120 << 30)
 
 
 class ClockSampler:
@@ -239,6 +243,12 @@ def _init_worker(spec, blocks, barrier):
         side = spec["side"]
         items = {k: opce.preprocess(opce.prnu_patterns(side, side, k, 1, spec["cameras"], spec["seed"])[0])
                  for k in keys}
+    elif app == "ncc":
+        from oracle import ncc as oncc
+        from oracle import pce as opce
+        side = spec["side"]
+        items = {k: oncc.preprocess(opce.prnu_patterns(side, side, k, 1, spec["cameras"], spec["seed"])[0])
+                 for k in keys}
     elif app == "gmm":
         from paper_2009_04755_b200.synthdata import particle
         items = {k: particle(k, spec["seed"]) for k in keys}
@@ -264,6 +274,9 @@ def _worker_step(count):
         if spec["app"] == "pce":
             from oracle import pce as opce
             opce.compare(items[i], items[j], spec["side"], spec["side"])
+        elif spec["app"] == "ncc":
+            from oracle import ncc as oncc
+            oncc.compare(items[i], items[j])
         elif spec["app"] == "gmm":
             from oracle import gmm as ogmm
             ogmm.compare(items[i], items[j], spec["angles"])
@@ -294,7 +307,7 @@ class CpuArm:
                 b = rng.randrange(0, max(1, n - self.block))
                 blocks.append([int(x) for x in sizes[b:b + self.block]])
         else:
-            self.block = 12 if args.app == "pce" else 24
+            self.block = 12 if args.app in ("pce", "ncc") else 24
             for _ in range(self.cores):
                 b = rng.randrange(0, max(1, n - self.block))
                 blocks.append(list(range(b, min(n, b + self.block))))
@@ -328,6 +341,8 @@ class CpuArm:
 def cpu_what(args):
     if args.app == "pce":
         return f"{args.side}x{args.side} PCE compares (numpy float64 irfft2 + peak/energy)"
+    if args.app == "ncc":
+        return f"{args.side}x{args.side} zero-lag NCC compares (numpy float64 dot of normalised items)"
     if args.app == "gmm":
         return f"particle-pair GMM costs (K={args.angles}, numpy float64)"
     return "composition-vector cosines (pure-Python merge of the reference's compare)"
@@ -430,6 +445,81 @@ def pce_parity(args, n, side, out, flags, items=None, gen_stream=None):
                       "of the peak) may take the peak at either location"}
 
 
+def ncc_parity(args, n, side, out, flags, items=None):
+    """Sampled pair ids of the finished NCC job against the float64 oracle (|err| <= 2e-4, TF32)."""
+    import numpy as np
+    import torch
+
+    from oracle import ncc as oncc
+    from oracle import scheduler as osch
+    from paper_2009_04755_b200 import device
+    f = flags.cpu().numpy()
+    mine = np.flatnonzero(f)
+    if len(mine) == 0:
+        return {"sampled": 0, "max_abs_err": None, "tolerance": 2e-4, "pass": False}
+    rng = np.random.default_rng(args.seed + 99)
+    pids = sorted(int(x) for x in rng.choice(mine, size=min(args.parity_samples, len(mine)), replace=False))
+    ss = side * side
+    buf = torch.empty(ss, dtype=torch.float32, device="cuda")
+    vec = {}
+    for p in pids:
+        for k in osch.pair_from_id(n, p):
+            if k not in vec:
+                if items is not None:
+                    x = items[k * ss:(k + 1) * ss].cpu().numpy()
+                else:
+                    device.synth_prnu(side, side, k, 1, args.cameras, args.seed, buf)
+                    x = buf.cpu().numpy()
+                vec[k] = oncc.preprocess(x)
+    want = np.array([oncc.compare(*(vec[k] for k in osch.pair_from_id(n, p))) for p in pids])
+    got = out.cpu().numpy()[pids]
+    err = float(np.max(np.abs(got - want)))
+    flags_ok = bool(np.all(np.where(got >= 0.02, f[pids] == 3, f[pids] == 1)))
+    return {"sampled": len(pids), "max_abs_err": err, "tolerance": 2e-4, "flags_match": flags_ok,
+            "pass": bool(err <= 2e-4 and flags_ok), "oracle": "oracle/ncc.py float64"}
+
+
+def calibrate_ncc(args, params_fn, side, cameras, seed):
+    """Isolated single-GPU NCC stage costs: t_pre per item (normalise), t_cmp per pair
+    of a resident Gram over m items (m large enough for > 1 wave of 256 x 256 tiles)."""
+    import torch
+
+    from paper_2009_04755_b200 import device
+    ss = side * side
+    free = torch.cuda.mem_get_info()[0]
+    m = int(min(args.items, 4096, (free - (24 << 30)) // (ss * 4)) // 256 * 256)
+    m = max(m, 256)
+    app = device.DeviceApp(params_fn(m))
+    slots = app.alloc_slots(m)
+    raw = torch.empty(256 * ss, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream()
+    t_pre = 0.0
+    for c0 in range(0, m, 256):
+        cnt = min(256, m - c0)
+        device.synth_prnu(side, side, c0, cnt, cameras, seed, raw)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        app.preprocess(raw, ss * 4, cnt, slots, list(range(c0, c0 + cnt)))
+        e1.record(s)
+        torch.cuda.synchronize()
+        t_pre += e0.elapsed_time(e1) / 1e3
+    del raw
+    out = torch.zeros(m * (m - 1) // 2, dtype=torch.float64, device="cuda")
+    app.gram(slots, m, out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(2):
+        app.gram(slots, m, out)
+    e1.record(s)
+    torch.cuda.synchronize()
+    t_cmp = e0.elapsed_time(e1) / 1e3 / (2 * m * (m - 1) // 2)
+    app.close()
+    del slots, out
+    torch.cuda.empty_cache()
+    return t_pre / m, t_cmp
+
+
 def calibrate_pce(args, params_fn, side, cameras, seed):
     """Isolated single-GPU stage costs for the perf model (perfmodel.py:99-114):
     t_pre = preprocess time per item, t_cmp = compare time per pair, each from
@@ -498,13 +588,18 @@ def main_pce(args, rank, world, local_rank):
     ss = side * side
     parsed_bytes = ss * 4
 
+    ncc = args.app == "ncc"
+
     def params_fn(m):
+        if ncc:
+            return _lib.app_params(_lib.APP_NCC, m, height=side, width=side, threshold=0.02)
         return _lib.app_params(_lib.APP_PCE, m, height=side, width=side, threshold=60.0)
 
     # isolated single-GPU stage costs (rank 0 alone on its GPU; the others wait)
     t_pre = t_cmp = None
     if rank == 0:
-        t_pre, t_cmp = calibrate_pce(args, params_fn, side, args.cameras, args.seed)
+        calib = calibrate_ncc if ncc else calibrate_pce
+        t_pre, t_cmp = calib(args, params_fn, side, args.cameras, args.seed)
     barrier()
 
     items = None
@@ -515,7 +610,7 @@ def main_pce(args, rank, world, local_rank):
     # N > 1: peer-GPU tier -- each rank preprocesses its home items (k % N == rank),
     # every other item it needs is copied from its home GPU over NVLink (CUDA IPC)
     peer = world > 1
-    steal = peer and not args.no_steal
+    steal = peer and not args.no_steal and not ncc     # the Gram deals its blocks statically
     if streamed:
         home_cnt = len(range(rank, n, world))
         free = torch.cuda.mem_get_info()[0]
@@ -523,6 +618,10 @@ def main_pce(args, rank, world, local_rank):
         # cache slots: what is left after the home region, T scratch and the result triangle
         budget = free - home_cnt * slot_bytes - pairs_total * 9 - (12 << 30)
         dslots = args.slots or max(64, int(budget // slot_bytes))
+        if ncc:   # two fetch buffers of (at most) 2,048 items: the Gram's key sub-blocks
+            dslots = args.slots or min(4096, int(budget // slot_bytes) // 256 * 256)
+    elif ncc and peer:
+        dslots = args.slots or min(4096, (n // world + 255) // 256 * 256 * 2)
     else:
         dslots = n
     eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=dslots, rank=rank, world=world,
@@ -619,7 +718,7 @@ def main_pce(args, rank, world, local_rank):
 
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = pce_parity(args, n, side, out, flags, items=items)
+        parity = (ncc_parity if ncc else pce_parity)(args, n, side, out, flags, items=items)
 
     # ---- e2e: pinned host patterns -> engine -> packed triangle back on host
     e2e = None
@@ -724,7 +823,22 @@ def main_pce(args, rank, world, local_rank):
             traffic_per_pair = None      # the capture is for another pattern size
     except Exception:
         traffic_per_pair = None
-    if ksamples:
+    if ncc:
+        # tensor-bound: 2 D flops per pair over the whole job (preprocess and fetches included)
+        tf32, tf32_src = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")) as fh:
+                tf32 = float(json.load(fh)["tf32"]["burst_tflops"])
+            tf32_src = "profiles/r2_tf32_peak.json (cuBLAS TF32 8192^3 on B200, burst)"
+        except Exception:
+            tf32 = 0.5 * float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+            tf32_src = "fallback: half the measured dense BF16 (MEASURED_PEAKS.json)"
+        achieved = 2.0 * ss * (all_pairs / max(1, args.steps)) / (ms / 1e3 / args.steps) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32 * world, "unit": "TFLOP/s",
+                    "frac": achieved / (tf32 * world), "traffic": None, "peak_source": tf32_src,
+                    "kernel": "ncc_gram2_kernel (tcgen05.mma.cta_group::2.kind::tf32, 256x256 item tiles, TMA)",
+                    "flops_per_pair": 2 * ss, "what": "whole job (normalise + fetches + Gram) per step"}
+    elif ksamples:
         per_launch_ms = kms / ksamples
         batch = kpairs / ksamples
         achieved = alg_bytes_per_pair * batch / (per_launch_ms / 1e3) / 1e9
@@ -946,7 +1060,7 @@ def main():
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
               f"(torchrun --nproc-per-node {args.gpus}) or drop torchrun and let --gpus relaunch", file=sys.stderr)
         return 2
-    if args.app != "pce":
+    if args.app not in ("pce", "ncc"):
         return main_app(args, rank, world, local_rank)
     return main_pce(args, rank, world, local_rank)
 

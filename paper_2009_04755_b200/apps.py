@@ -321,6 +321,22 @@ class PCEApp(B200Application):
         return out
 
 
+class NCCApp(PCEApp):
+    """Zero-lag normalised cross-correlation of fp32 patterns (the paper's forensics
+    compare): preprocess normalises each item to zero mean and unit
+    norm, compare is the dot product -- all pairs run as a tcgen05 TF32 Gram
+    (|error| <= 2e-4).  Same pattern I/O as PCEApp; match = NCC >= threshold."""
+
+    name = "ncc"
+    kind = _lib.APP_NCC
+
+    def __init__(self, n: int, side: int = 1024, *, threshold: Optional[float] = 0.02, **kw):
+        super().__init__(n, side, threshold=threshold, **kw)
+
+    def _slot_bytes(self) -> int:
+        return self.side * self.side * 4          # D normalised fp32 samples
+
+
 class SyntheticApp(B200Application):
     """The reference's SyntheticApp (apps.py:154-227) with the hash compare on the GPU.
 

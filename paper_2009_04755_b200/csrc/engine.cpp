@@ -342,6 +342,9 @@ struct rk_engine {
   int ev_used = 0;
   // exactly-once ledger: own region in the arena allocation; marks go to `ledger_target`
   // (own, or rank 0's region mapped over IPC when the job shares one ledger)
+  // NCC Gram over the peer tier: one compute stream per home sub-block, fetch events
+  std::vector<cudaStream_t> gstreams;
+  std::vector<cudaEvent_t> gevents;
   size_t ledger_off = 0;
   size_t ledger_bytes = 0;
   void* ledger_own = nullptr;
@@ -565,6 +568,124 @@ rk_status ncc_blocked_run(rk_engine* e, const void* h_parsed, const void* d_pars
   return RK_OK;
 }
 
+// NCC Gram over the peer tier (distcache.py owner_of(k) = k mod p for the Gram's
+// key blocks).  Rank s's home items (keys s + m*world, home slots m) are cut into
+// sub-blocks of B items, B = half the cache arena; all M sub-blocks of the job in
+// (t, s) order.  Every unordered pair of sub-blocks {a, b} (a = b included) is one
+// Gram block, computed by the owner of a when b lies in the circulant half after a
+// (b - a mod M in [1, M/2), the diametric pair by the lower index), so every rank
+// gets the same number of blocks.  A rank walks its partner sub-blocks b: a home
+// b is read in place, any other is copied from its owner's home region over
+// NVLink (CUDA IPC) into one of two fetch buffers on the load stream while the
+// previous partner's blocks multiply -- the blocks of one partner run on one
+// stream per home sub-block so together they fill the SMs.
+rk_status ncc_peer_run(rk_engine* e, double* d_out, uint8_t* d_flags, int64_t launches0) {
+  const int32_t n = e->app->p.n, w = e->p.world, r = e->p.rank;
+  const int grp = std::max(1, e->app->slot_group);
+  const int32_t B = (int32_t)(e->arena_slots / 2) / grp * grp;
+  if (B < grp)
+    return set_error(RK_ERR_NO_EVICTABLE, "NCC over the peer tier needs >= %d device slots (have %zu)", 2 * grp,
+                     e->arena_slots);
+  struct Sub {
+    int32_t s, m0, cnt;
+  };
+  std::vector<Sub> subs;
+  auto home_cnt = [&](int32_t s) { return n > s ? (n - s + w - 1) / w : 0; };
+  int32_t tmax = 0;
+  for (int32_t s = 0; s < w; ++s) tmax = std::max(tmax, (home_cnt(s) + B - 1) / B);
+  for (int32_t t = 0; t < tmax; ++t)
+    for (int32_t s = 0; s < w; ++s)
+      if (t * B < home_cnt(s)) subs.push_back(Sub{s, t * B, std::min(B, home_cnt(s) - t * B)});
+  const int M = (int)subs.size();
+  std::vector<int> mine;
+  for (int a = 0; a < M; ++a)
+    if (subs[a].s == r) mine.push_back(a);
+  // partner b -> the home sub-blocks a that pair with it on this rank
+  std::vector<std::vector<int>> with(M);
+  for (int a : mine) {
+    with[a].push_back(a);
+    for (int dd = 1; 2 * dd <= M; ++dd) {
+      const int b = (a + dd) % M;
+      if (2 * dd < M || a < b) with[b].push_back(a);
+    }
+  }
+  // partners: home ones first (no copy), then the fetched ones in circulant order
+  std::vector<int> order;
+  for (int b = 0; b < M; ++b)
+    if (!with[b].empty() && subs[b].s == r) order.push_back(b);
+  for (int dd = 1; dd < M; ++dd)
+    for (int a0 : {mine.empty() ? 0 : mine[0]}) {
+      const int b = (a0 + dd) % M;
+      if (!with[b].empty() && subs[b].s != r) order.push_back(b);
+    }
+  const size_t stride = e->slot_stride;
+  while ((int)e->gstreams.size() < (int)mine.size()) {
+    cudaStream_t st;
+    RK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    e->gstreams.push_back(st);
+  }
+  // events: 2 fetch-done + per buffer and stream one use-done
+  const size_t need_ev = 2 + 2 * e->gstreams.size() + 1;
+  while (e->gevents.size() < need_ev) {
+    cudaEvent_t ev;
+    RK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->gevents.push_back(ev);
+  }
+  cudaEvent_t* ev_fetched = &e->gevents[0];
+  cudaEvent_t* ev_used = &e->gevents[2];            // [buf * S + stream]
+  cudaEvent_t ev_start = e->gevents[need_ev - 1];
+  const int S = (int)e->gstreams.size();
+  RK_CUDA(cudaEventRecord(ev_start, e->stream));
+  for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamWaitEvent(e->gstreams[q], ev_start, 0));
+  RK_CUDA(cudaStreamWaitEvent(e->lstream, ev_start, 0));
+  std::vector<int> slot_stream(M, -1);
+  for (int q = 0; q < (int)mine.size(); ++q) slot_stream[mine[q]] = q;
+  int nf = 0;
+  for (int b : order) {
+    int32_t brow;
+    if (subs[b].s == r) {
+      brow = (int32_t)e->arena_slots + subs[b].m0;
+    } else {
+      const int f = nf % 2;
+      if (nf >= 2)   // buffer f's previous partner is multiplied on every stream
+        for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamWaitEvent(e->lstream, ev_used[f * S + q], 0));
+      const int tk = trace_begin(e, 2, subs[b].s + subs[b].m0 * w, -1, subs[b].cnt, e->lstream);
+      RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + (size_t)f * B * stride,
+                              e->peer_home[subs[b].s] + (size_t)subs[b].m0 * stride, (size_t)subs[b].cnt * stride,
+                              cudaMemcpyDeviceToDevice, e->lstream));
+      trace_end(e, tk, e->lstream);
+      RK_CUDA(cudaEventRecord(ev_fetched[f], e->lstream));
+      for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamWaitEvent(e->gstreams[q], ev_fetched[f], 0));
+      e->stats.peer_fetches += subs[b].cnt;
+      e->stats.peer_bytes += (int64_t)subs[b].cnt * (int64_t)stride;
+      brow = f * B;
+      ++nf;
+    }
+    for (int a : with[b]) {
+      const int q = slot_stream[a];
+      const int tk = trace_begin(e, 0, subs[a].s + subs[a].m0 * w, subs[b].s + subs[b].m0 * w,
+                                 a == b ? subs[a].cnt * (subs[a].cnt - 1) / 2 : subs[a].cnt * subs[b].cnt,
+                                 e->gstreams[q]);
+      RK_TRY(ncc_gram_block_strided(e->app, e->arena, stride, (int32_t)(e->arena_slots + e->home_slots),
+                                    (int32_t)e->arena_slots + subs[a].m0, subs[a].s + subs[a].m0 * w, subs[a].cnt,
+                                    brow, subs[b].s + subs[b].m0 * w, subs[b].cnt, w, a == b, d_out, d_flags,
+                                    e->gstreams[q]));
+      trace_end(e, tk, e->gstreams[q]);
+      e->stats.pairs_done += a == b ? (int64_t)subs[a].cnt * (subs[a].cnt - 1) / 2
+                                    : (int64_t)subs[a].cnt * subs[b].cnt;
+      e->stats.tiles += 1;
+    }
+    if (subs[b].s != r)
+      for (int q = 0; q < S; ++q) RK_CUDA(cudaEventRecord(ev_used[((nf - 1) % 2) * S + q], e->gstreams[q]));
+  }
+  for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamSynchronize(e->gstreams[q]));
+  RK_CUDA(cudaStreamSynchronize(e->lstream));
+  RK_CUDA(cudaStreamSynchronize(e->stream));
+  RK_TRY(trace_collect(e));
+  e->stats.kernel_launches += e->app->launches - launches0;
+  return RK_OK;
+}
+
 extern "C" {
 
 rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_params* params, int device,
@@ -597,8 +718,11 @@ rk_status rk_engine_create(const rk_app_params* app_params, const rk_engine_para
   ce = cudaEventCreateWithFlags(&e->ev_loaded, cudaEventDisableTiming);
   if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->ev_compared, cudaEventDisableTiming);
   if (ce != cudaSuccess) return fail(check_cuda(ce, "cudaEventCreate"));
-  if (params->peer_tier && params->world > 1)
-    e->home_slots = (app_params->n + params->world - 1) / params->world;
+  if (params->peer_tier && params->world > 1) {
+    // whole slot groups, so the home region is a block of rows of the Gram's tensor map
+    const int g = std::max(1, e->app->slot_group);
+    e->home_slots = ((app_params->n + params->world - 1) / params->world + g - 1) / g * g;
+  }
   // interleaved slot groups (rk_app_slot_group): whole groups only
   const size_t g = (size_t)std::max(1, e->app->slot_group);
   e->arena_slots = ((size_t)params->device_slots + g - 1) / g * g;
@@ -648,6 +772,8 @@ void rk_engine_destroy(rk_engine* e) {
   if (e->ev_compared) cudaEventDestroy(e->ev_compared);
   for (cudaEvent_t ev : e->ev_chunk)
     if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t st : e->gstreams) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : e->gevents) cudaEventDestroy(ev);
   if (e->cstream) cudaStreamDestroy(e->cstream);
   if (e->h_qres) cudaFreeHost(e->h_qres);
   cudaFree(e->arena);
@@ -729,8 +855,14 @@ static rk_status engine_run_impl(rk_engine* e, const void* h_parsed, const void*
   RK_CUDA(cudaStreamWaitEvent(e->lstream, e->ev_compared, 0));
   e->loads_unsynced = false;
   if (e->app->p.kind == RK_APP_NCC) {
-    // Gram path: every item resident in slot == key, then one tcgen05 GEMM over
-    // this rank's upper-triangle tiles
+    // Gram path over the peer tier: home items resident, others fetched over NVLink
+    if (e->home_slots > 0) {
+      if (!e->peers_ready)
+        return set_error(RK_ERR_VALUE, "peer tier: call rk_engine_load_home and rk_engine_set_peer_homes first");
+      return ncc_peer_run(e, d_out, d_flags, launches0);
+    }
+    // every item resident in slot == key, then one tcgen05 GEMM over this rank's
+    // upper-triangle tiles
     if (e->tier->capacity < n) return ncc_blocked_run(e, h_parsed, d_parsed, parsed_stride, d_out, d_flags, launches0);
     std::vector<LoadReq> all;
     for (int32_t k = 0; k < n; ++k) {

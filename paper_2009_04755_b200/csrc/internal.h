@@ -63,6 +63,29 @@ __device__ __forceinline__ void ledger_mark(const LedgerRef& L, int64_t pid) {
     atomicCAS_system(L.ctr + 1, 0ull, (unsigned long long)pid + 1ull);
   }
 }
+// Marks of a thread's pair ids in ascending order (a tile row's columns), one
+// atomicOr per 32-bit word of the bitmap touched: add() each id, flush() at the end.
+struct LedgerRun {
+  int64_t word;
+  uint32_t mask;
+};
+__device__ __forceinline__ void ledger_run_flush(const LedgerRef& L, LedgerRun& r) {
+  if (L.bits != nullptr && r.mask != 0u) {
+    const uint32_t dup = atomicOr_system(L.bits + r.word, r.mask) & r.mask;
+    if (dup) {
+      atomicAdd_system(L.ctr, (unsigned long long)__popc(dup));
+      atomicCAS_system(L.ctr + 1, 0ull, (unsigned long long)(r.word * 32 + __ffs(dup) - 1) + 1ull);
+    }
+  }
+  r.mask = 0u;
+}
+__device__ __forceinline__ void ledger_run_add(const LedgerRef& L, LedgerRun& r, int64_t pid) {
+  if ((pid >> 5) != r.word) {
+    ledger_run_flush(L, r);
+    r.word = pid >> 5;
+  }
+  r.mask |= 1u << (uint32_t)(pid & 31);
+}
 // `cnt` consecutive pair ids from pid0 (a tile row's run of columns): one
 // atomicOr per 32-bit word instead of one per pair.
 __device__ __forceinline__ void ledger_mark_run(const LedgerRef& L, int64_t pid0, int cnt) {
@@ -166,6 +189,10 @@ int ncc_gram_tile(int n);
 rk_status ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
                          int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt, double* d_out,
                          uint8_t* d_flags, cudaStream_t s);
+
+rk_status ncc_gram_block_strided(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                                 int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt,
+                                 int32_t kstep, bool tri, double* d_out, uint8_t* d_flags, cudaStream_t s);
 
 rk_status pce_compare_list(rk_app* app, const void* d_slots, size_t slot_stride, const rk_pair* pairs, int n,
                            double* d_out, uint8_t* d_flags, cudaStream_t s);

@@ -349,11 +349,17 @@ constexpr int kChunkBlocks = NCC_KCHUNK;   // k-blocks (x 32 floats) per launch:
 // tiles only).  Tiles t with t % world == rank are computed.  Slot rows must be
 // multiples of 128 (the interleaved slot groups).  The all-resident Gram is the
 // block (0, 0, n) x (0, 0, n).
+// Block of the Gram: A = arena rows a_row0 .. a_row0+a_cnt-1 holding keys
+// a_key0 + r*a_kstep (likewise B).  tri: A == B, pairs lc > lr; otherwise every
+// (lr, lc) is a pair, stored at pair_id(min(i, j), max(i, j)).  kstep 1: contiguous
+// key blocks; kstep = world: one rank's home items (key = rank + m*world, the
+// peer tier's point of contact k mod world).
 struct GramBlock {
   int a_row0, a_key0, a_cnt;
   int b_row0, b_key0, b_cnt;
   int tri, rank, world;
   int na, nb;   // 256-item tiles along A and B
+  int a_kstep, b_kstep;
 };
 
 // One CTA pair (cluster of 2) per 256x256 tile of a Gram block.
@@ -459,28 +465,31 @@ __global__ void __launch_bounds__(kGramThreads, 1) ncc_gram2_kernel(const __grid
   mbar_wait(&done_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int lr = lrow0 + warp * 32 + lane;
-  const int i = blk.a_key0 + lr;
+  const int i = blk.a_key0 + lr * blk.a_kstep;
   const int64_t nn = n;
 #pragma unroll 1
   for (int c = 0; c < kTile2; c += 32) {
     float r[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
     if (lr < blk.a_cnt) {
+      const bool last = (int64_t)kb1 * kBK >= d;   // the pairs complete with their last K chunk
+      LedgerRun run{-1, 0u};
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const int lc = lcol0 + c + k;
-        const int j = blk.b_key0 + lc;
-        if (lc < blk.b_cnt && j > i) {
-          const int64_t pid = (int64_t)i * (2 * nn - i - 1) / 2 + (j - i - 1);
+        if (lc < blk.b_cnt && (!blk.tri || lc > lr)) {
+          const int j = blk.b_key0 + lc * blk.b_kstep;
+          const int lo = min(i, j), hi = max(i, j);
+          const int64_t pid = (int64_t)lo * (2 * nn - lo - 1) / 2 + (hi - lo - 1);
           const double v = first ? (double)r[k] : out[pid] + (double)r[k];
           out[pid] = v;
-          if (flags && (int64_t)kb1 * kBK >= d) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
+          if (last) {
+            if (flags) flags[pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (v >= threshold ? 2 : 0));
+            ledger_run_add(ledger, run, pid);
+          }
         }
       }
-      if ((int64_t)kb1 * kBK >= d) {   // the pairs complete with their last K chunk
-        const int l0 = max(lcol0 + c, i + 1 - blk.b_key0), l1 = min(lcol0 + c + 32, blk.b_cnt);
-        if (l1 > l0) ledger_mark_run(ledger, (int64_t)i * (2 * nn - i - 1) / 2 + (blk.b_key0 + l0 - i - 1), l1 - l0);
-      }
+      ledger_run_flush(ledger, run);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -639,7 +648,26 @@ rk_status ncc_gram_block(rk_app* app, const void* d_slots, size_t slot_stride, i
   CUtensorMap map;
   RK_TRY(gram_tensor_map(app, d_slots, slot_stride, n_rows, &map));
   GramBlock blk{a_row0, a_key0, a_cnt, b_row0, b_key0, b_cnt, tri ? 1 : 0, 0, 1,
-                (a_cnt + kTile2 - 1) / kTile2, (b_cnt + kTile2 - 1) / kTile2};
+                (a_cnt + kTile2 - 1) / kTile2, (b_cnt + kTile2 - 1) / kTile2, 1, 1};
+  return gram_block_launch(app, map, blk, d_out, d_flags, s);
+}
+
+// Strided-key block (the engine's peer-tier NCC path): A = rows a_row0.. holding
+// keys a_key0 + r*kstep, B likewise; tri = A is B.  The caller guarantees
+// disjoint key sets for distinct blocks.
+rk_status ncc_gram_block_strided(rk_app* app, const void* d_slots, size_t slot_stride, int32_t n_rows, int32_t a_row0,
+                                 int32_t a_key0, int32_t a_cnt, int32_t b_row0, int32_t b_key0, int32_t b_cnt,
+                                 int32_t kstep, bool tri, double* d_out, uint8_t* d_flags, cudaStream_t s) {
+  if (a_row0 % kGroup || b_row0 % kGroup)
+    return set_error(RK_ERR_VALUE, "Gram block rows must start on a slot group (%d)", kGroup);
+  if (a_cnt <= 0 || b_cnt <= 0 || a_row0 + a_cnt > n_rows || b_row0 + b_cnt > n_rows || kstep < 1)
+    return set_error(RK_ERR_VALUE, "Gram block outside the arena");
+  if (a_key0 + (int64_t)(a_cnt - 1) * kstep >= app->p.n || b_key0 + (int64_t)(b_cnt - 1) * kstep >= app->p.n)
+    return set_error(RK_ERR_VALUE, "Gram block keys outside [0, n)");
+  CUtensorMap map;
+  RK_TRY(gram_tensor_map(app, d_slots, slot_stride, n_rows, &map));
+  GramBlock blk{a_row0, a_key0, a_cnt, b_row0, b_key0, b_cnt, tri ? 1 : 0, 0, 1,
+                (a_cnt + kTile2 - 1) / kTile2, (b_cnt + kTile2 - 1) / kTile2, kstep, kstep};
   return gram_block_launch(app, map, blk, d_out, d_flags, s);
 }
 
@@ -668,7 +696,7 @@ rk_status ncc_gram(rk_app* app, const void* d_slots, size_t slot_stride, int32_t
 #ifndef NCC_GRAM_1CTA
   if (ncc_gram_tile(n) == kTile2) {
     const int side = (n + kTile2 - 1) / kTile2;
-    GramBlock blk{0, 0, n, 0, 0, n, 1, rank, world, side, side};
+    GramBlock blk{0, 0, n, 0, 0, n, 1, rank, world, side, side, 1, 1};
     return gram_block_launch(app, map, blk, d_out, d_flags, s);
   }
 #endif

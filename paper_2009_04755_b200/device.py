@@ -83,6 +83,12 @@ class DeviceApp:
         check(lib.rk_ledger_read(_ptr(region), self.params.n, C.byref(st)))
         return st.as_dict()
 
+    def gram(self, slots: torch.Tensor, n_rows: int, out: torch.Tensor, flags: Optional[torch.Tensor] = None,
+             rank: int = 0, world: int = 1, stream=None) -> None:
+        """NCC all-pairs over resident slots (slot k = item k) as the tcgen05 Gram (rk_ncc_gram)."""
+        check(lib.rk_ncc_gram(self.handle, _ptr(slots), self.slot_stride, n_rows, rank, world, _ptr(out),
+                              _ptr(flags), _stream(stream)))
+
     def compare_tile(self, slots: Optional[torch.Tensor], r0: int, r1: int, c0: int, c1: int,
                      slot_of_key: Sequence[int], out: torch.Tensor, flags: Optional[torch.Tensor] = None,
                      stream=None) -> None:

@@ -115,7 +115,7 @@ class AllPairsEngine:
         slots = device_slots if device_slots is not None else app.n
         self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
                                  rank=rank, world=world, device=app.device,
-                                 peer_tier=peer_tier and world > 1 and app.kind not in (0, 3),
+                                 peer_tier=peer_tier and world > 1 and app.kind != 0,
                                  steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk,
                                  host_slots=host_slots)
         self._peers_connected = False

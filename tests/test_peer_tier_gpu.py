@@ -115,3 +115,58 @@ def test_ranks_steal_from_a_late_rank(world, n):
     assert sum(o[3]["loads"] for o in outs) == n                 # every item preprocessed once, on its home rank
     led = outs[0][3]["ledger"]
     assert led["full"] == 1 and led["completed"] == total and led["dup_marks"] == 0
+
+
+def _ncc_rank(rank, world, port, ret, n, side, slots):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2009_04755_b200.apps import NCCApp
+        from paper_2009_04755_b200.engine import AllPairsEngine
+        app = NCCApp(n, side=side, cameras=4, seed=41, device=0)
+        eng = AllPairsEngine(app, device_slots=slots, rank=rank, world=world)
+        res = eng.run(gather=False)
+        ret.put((rank, res.values.copy(), res.flags.copy(), dict(res.stats, ledger=res.ledger)))
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,side,slots", [(2, 600, 128, 256), (3, 700, 512, 256)])
+def test_ncc_gram_over_the_peer_tier(world, n, side, slots):
+    """NCC all-pairs through the public engine with the peer tier (ranks sharing
+    cuda:0 over CUDA IPC): each rank normalises only its home items (k % world),
+    cuts them into sub-blocks of half its cache arena, and multiplies its share of
+    the sub-block pairs, copying every non-home partner from its owner's home
+    region.  side 512 = two K chunks per block.  Every pair once (flags and the
+    shared device ledger), TF32 Gram within 2e-4 of the float64 oracle."""
+    import torch.multiprocessing as mp
+    from oracle import ncc as oncc
+    from paper_2009_04755_b200.apps import NCCApp
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ncc_rank, args=(r, world, port, ret, n, side, slots)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([ret.get(timeout=600) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    total = n * (n - 1) // 2
+    values = sum(o[1] for o in outs)
+    flags = sum(o[2].astype(np.int32) for o in outs)
+    assert set(np.unique(flags)) <= {1, 3}
+    app = NCCApp(n, side=side, cameras=4, seed=41)
+    pats = np.stack([np.frombuffer(app.fetch_raw(app.path_for_key(k)), dtype=np.float32) for k in range(n)])
+    assert np.max(np.abs(values - oncc.all_pairs_chunked(pats))) <= 2e-4
+    assert sum(o[3]["pairs_done"] for o in outs) == total
+    assert sum(o[3]["loads"] for o in outs) == n                  # home items only: R = 1
+    assert all(o[3]["peer_fetches"] > 0 for o in outs)
+    pairs = [o[3]["pairs_done"] for o in outs]
+    assert max(pairs) <= 2 * min(pairs)                           # circulant share: balanced
+    led = outs[0][3]["ledger"]
+    assert led["full"] == 1 and led["completed"] == total and led["dup_marks"] == 0
