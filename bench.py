@@ -533,24 +533,37 @@ def calibrate_pce(args, params_fn, side, cameras, seed):
     raw = torch.empty(m * ss, dtype=torch.float32, device="cuda")
     device.synth_prnu(side, side, 0, m, cameras, seed, raw)
     slots = app.alloc_slots(m)
-    pairs = [(i, j, i, j) for i in range(m) for j in range(i + 1, m)]
+    import ctypes as C
+
+    from paper_2009_04755_b200 import _lib
+    plist = [(i, j, i, j) for i in range(m) for j in range(i + 1, m)]
+    pairs = (_lib.Pair * len(plist))(*[_lib.Pair(*p) for p in plist])   # built once: no host gaps
     out = torch.zeros(m * (m - 1) // 2, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()
-    app.preprocess(raw, ss * 4, m, slots, list(range(m)))
-    app.compare_pairs(slots, pairs, out)
+    idx = (C.c_int32 * m)(*range(m))
+
+    def pre():
+        _lib.check(_lib.lib.rk_preprocess(app.handle, raw.data_ptr(), ss * 4, m, slots.data_ptr(), app.slot_stride,
+                                          idx, s.cuda_stream))
+
+    def cmp():
+        _lib.check(_lib.lib.rk_compare_pairs(app.handle, slots.data_ptr(), app.slot_stride, pairs, len(plist),
+                                             out.data_ptr(), None, s.cuda_stream))
+    pre()
+    cmp()
     torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     e[0].record(s)
     for _ in range(3):
-        app.preprocess(raw, ss * 4, m, slots, list(range(m)))
+        pre()
     e[1].record(s)
     e[2].record(s)
     for _ in range(3):
-        app.compare_pairs(slots, pairs, out)
+        cmp()
     e[3].record(s)
     torch.cuda.synchronize()
     t_pre = e[0].elapsed_time(e[1]) / 1e3 / (3 * m)
-    t_cmp = e[2].elapsed_time(e[3]) / 1e3 / (3 * len(pairs))
+    t_cmp = e[2].elapsed_time(e[3]) / 1e3 / (3 * len(plist))
     app.close()
     del raw, slots, out
     torch.cuda.empty_cache()

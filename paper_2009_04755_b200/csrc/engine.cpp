@@ -650,8 +650,11 @@ rk_status ncc_peer_run(rk_engine* e, double* d_out, uint8_t* d_flags, int64_t la
       if (nf >= 2)   // buffer f's previous partner is multiplied on every stream
         for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamWaitEvent(e->lstream, ev_used[f * S + q], 0));
       const int tk = trace_begin(e, 2, subs[b].s + subs[b].m0 * w, -1, subs[b].cnt, e->lstream);
+      // whole slot groups: the NCC layout interleaves each group's 128 items ([D/1024][128][1024]),
+      // so a partial group is not a byte prefix (home regions are allocated in whole groups)
+      const size_t rows = (size_t)(subs[b].cnt + grp - 1) / grp * grp;
       RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + (size_t)f * B * stride,
-                              e->peer_home[subs[b].s] + (size_t)subs[b].m0 * stride, (size_t)subs[b].cnt * stride,
+                              e->peer_home[subs[b].s] + (size_t)subs[b].m0 * stride, rows * stride,
                               cudaMemcpyDeviceToDevice, e->lstream));
       trace_end(e, tk, e->lstream);
       RK_CUDA(cudaEventRecord(ev_fetched[f], e->lstream));
