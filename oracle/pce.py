@@ -50,33 +50,6 @@ def pce_from_plane(c: np.ndarray) -> tuple[float, float, int]:
     return peak * abs(peak) / energy, peak, p
 
 
-def pce_candidates(c: np.ndarray, rtol: float = 1e-5) -> np.ndarray:
-    """PCE with the peak taken at every location whose value is within `rtol` of
-    the maximum (the argmax's own PCE first).  The float64 plane and the device's
-    fp32 plane agree to ~1e-6 of the peak, so when two separate locations are that
-    close the argmax -- and with it the excluded 11 x 11 window -- is not defined
-    by the arithmetic; parity accepts the PCE of any such near-tie."""
-    h, w = c.shape
-    p0 = int(np.argmax(c))
-    top = float(c.flat[p0])
-    locs = [p0] + [int(p) for p in np.flatnonzero(c >= top - rtol * abs(top)) if int(p) != p0]
-    total = float(np.sum(c * c))
-    out = []
-    for p in locs:
-        r, q = divmod(p, w)
-        rows = np.arange(r - WIN // 2, r + WIN // 2 + 1) % h
-        cols = np.arange(q - WIN // 2, q + WIN // 2 + 1) % w
-        win = c[np.ix_(rows, cols)]
-        peak = float(c.flat[p])
-        out.append(peak * abs(peak) / ((total - float(np.sum(win * win))) / (h * w - WIN * WIN)))
-    return np.array(out)
-
-
-def matches(got: float, cands: np.ndarray, rtol: float) -> bool:
-    """`got` equals (to rtol) the PCE of the argmax or of a near-tie (pce_candidates)."""
-    return bool(np.any(np.abs(got - cands) <= rtol * np.abs(cands)))
-
-
 def compare(si: np.ndarray, sj: np.ndarray, h: int, w: int) -> float:
     return pce_from_plane(correlation(si, sj, h, w))[0]
 
@@ -117,12 +90,11 @@ def prnu_patterns(h: int, w: int, first_key: int, n_items: int, cameras: int, se
     return out
 
 
-def pairs_batched(items: np.ndarray, pairs, batch: int = 16, workers: int = -1, candidates: bool = False):
+def pairs_batched(items: np.ndarray, pairs, batch: int = 16, workers: int = -1):
     """PCE of the listed (i, j) pairs over items[n, h, w] -- the same definition as
     ``compare`` (float64 throughout), with the inverse FFTs batched through
     scipy.fft on all host threads so parity tests can check thousands of 1024^2
-    pairs in seconds.  Spectra are computed once per distinct key.  With
-    candidates=True, a list of pce_candidates arrays (argmax PCE first)."""
+    pairs in seconds.  Spectra are computed once per distinct key."""
     import scipy.fft as sfft
     n, h, w = items.shape
     keys = sorted({k for p in pairs for k in p})
@@ -130,14 +102,11 @@ def pairs_batched(items: np.ndarray, pairs, batch: int = 16, workers: int = -1, 
     for k in keys:
         x = np.asarray(items[k], dtype=np.float64)
         spec[k] = sfft.rfft2(x - x.mean(), workers=workers)
-    out = [] if candidates else np.empty(len(pairs), dtype=np.float64)
+    out = np.empty(len(pairs), dtype=np.float64)
     for b0 in range(0, len(pairs), batch):
         chunk = pairs[b0:b0 + batch]
         prod = np.stack([spec[i] * np.conj(spec[j]) for i, j in chunk])
         planes = sfft.irfft2(prod, s=(h, w), workers=workers)
         for q in range(len(chunk)):
-            if candidates:
-                out.append(pce_candidates(planes[q]))
-            else:
-                out[b0 + q] = pce_from_plane(planes[q])[0]
+            out[b0 + q] = pce_from_plane(planes[q])[0]
     return out

@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
 #if PCE_WARP_COLS
         __syncwarp();                  // this warp's columns are consumed
         if (wl == 0 && c0 + 4 * kNG < cend) {
+          refill_fence();
           mbar_expect_tx(wbar, 2 * kWarpBytes);
           bulk_g2s_hint(wx, Xs + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);
           bulk_g2s_hint(wy, Ys + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);

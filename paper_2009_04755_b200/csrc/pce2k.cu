@@ -463,13 +463,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         ph ^= 2u;
         block8_rows_z<R>(e, gb, gi, lane);
         named_bar(1 + wg, kGW * 32);
-        if (leader && rb + 2 < kBlocks) issue(rb + 2, 0);
+        if (leader && rb + 2 < kBlocks) {
+          refill_fence();   // the group's generic reads of this buffer before the async refill
+          issue(rb + 2, 0);
+        }
         PCE2K_FFT(e);
         mbar_wait(&s_bar[wg][2], (ph >> 2) & 1u);
         ph ^= 4u;
         half_rows_zodd(o, gb + kUnitF2, gi, lane);
         named_bar(1 + wg, kGW * 32);
-        if (leader && rb + 2 < kBlocks) issue(rb + 2, 1);
+        if (leader && rb + 2 < kBlocks) {
+          refill_fence();
+          issue(rb + 2, 1);
+        }
         PCE2K_FFT(o);
         radix2_last<true>(e, o, wl);
         argmax2k_update(e, o, 8 * rb + 2 * gi, lane, m, idx, ss);

@@ -14,16 +14,20 @@ constexpr int kWin = 11;                // PCE exclusion neighbourhood side
 constexpr int kHalfWin = kWin / 2;
 constexpr int kMeanParts = 64;          // CTAs per item in the mean reduction
 
-// Refilling a staging buffer that was only READ by generic loads (the values are
-// already in registers, ordered by the group barrier) needs no proxy fence: the
-// generic -> async proxy fence is only required after generic WRITES.  ncu put
-// ~8 % of the compare kernel's stall samples on these per-refill fences (they
-// also wait for the leader's outstanding T stores).  -DPCE_REFILL_FENCE=1 restores them.
+// Refilling a staging buffer that other threads have just READ with generic
+// loads: the barrier before the refill orders the loads' issue, not their
+// completion, so the TMA (async proxy) write can overtake a load still in flight
+// (measured: without a fence 2-3 of 2,556 PCE values per 256^2 job differed from
+// run to run, up to 5e-4 relative; tools/pce_determinism.py).  The issuing thread
+// therefore fences generic -> async proxy on shared memory before every refill
+// (1, default: fence.proxy.async.shared::cta; 2: the full fence.proxy.async;
+// 0: none -- racy, kept only for the A/B record in DESIGN.md).
 #ifndef PCE_REFILL_FENCE
-#define PCE_REFILL_FENCE 0
+#define PCE_REFILL_FENCE 1
 #endif
 __device__ __forceinline__ void refill_fence() {
-  if (PCE_REFILL_FENCE) fence_proxy_async();
+  if (PCE_REFILL_FENCE == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (PCE_REFILL_FENCE == 2) fence_proxy_async();
 }
 
 // Row-phase unpack and energy sums on packed pairs (with RK_F32X2).

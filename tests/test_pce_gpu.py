@@ -16,16 +16,6 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-4
 
 
-def assert_pce_parity(got, cands, rtol=RTOL):
-    """Every device value equals the oracle's PCE at its argmax -- or, where the
-    float64 plane has another location within 1e-5 of the peak, the PCE at that
-    near-tie (oracle/pce.py pce_candidates).  Near-ties are rare and counted."""
-    bad = [k for k, c in enumerate(cands) if not opce.matches(float(got[k]), c, rtol)]
-    assert not bad, [(k, float(got[k]), cands[k].tolist()) for k in bad[:8]]
-    ties = sum(1 for k, c in enumerate(cands) if not opce.matches(float(got[k]), c[:1], rtol))
-    return ties
-
-
 def _lib():
     from paper_2009_04755_b200 import _lib, device
     return _lib, device
@@ -287,10 +277,9 @@ def test_engine_bench_path_many_pairs_per_cta(side, n, cams):
     assert total / launches >= 4 * sms, (total, launches, sms)
     host = items.cpu().numpy().reshape(n, side, side)
     pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
-    cands = opce.pairs_batched(host, pairs, candidates=True)
+    want = opce.pairs_batched(host, pairs)
     got = out.cpu().numpy()
-    ties = assert_pce_parity(got, cands)
-    assert ties <= max(2, total // 500)      # near-ties are rare: not a systematic offset
+    np.testing.assert_allclose(got, want, rtol=RTOL)
     f = flags.cpu().numpy()
     assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))
     st = eng.stats()
@@ -320,8 +309,8 @@ def test_2048_many_pairs_per_cta_sampled():
     from oracle import scheduler as osch
     pairs = [osch.pair_from_id(n, int(p)) for p in pids]
     host = items.cpu().numpy().reshape(n, side, side)
-    cands = opce.pairs_batched(host, pairs, batch=4, candidates=True)
-    assert_pce_parity(got[pids], cands)
+    want = opce.pairs_batched(host, pairs, batch=4)
+    np.testing.assert_allclose(got[pids], want, rtol=RTOL)
     f = flags.cpu().numpy()
     assert np.array_equal(f == 3, got >= 60.0) and np.all((f == 1) | (f == 3))
 
@@ -359,3 +348,24 @@ def test_engine_host_tier_write_through(host_slots):
             assert st["loads"] == n and st["host_evictions"] == 0     # R = 1
         else:
             assert st["loads"] > n and st["host_evictions"] > 0
+
+
+@pytest.mark.parametrize("side,n,runs", [(256, 72, 4), (1024, 40, 2)])
+def test_compare_is_deterministic_run_to_run(side, n, runs):
+    """The same job, run repeatedly with many pairs per persistent CTA, is
+    bit-identical: no staging buffer is refilled (TMA, async proxy) while another
+    thread's generic loads of it may still be in flight (tools/pce_determinism.py
+    found 2-3 of 2,556 values differing before the refill proxy fences)."""
+    _l, device = _lib()
+    items = make_items(n, side, cameras=6, seed=17)
+    total = n * (n - 1) // 2
+    outs = []
+    for _ in range(runs):
+        eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=8,
+                                  device_slots=n)
+        out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+        eng.run(out, device_items=items, parsed_stride=side * side * 4)
+        outs.append(out.cpu().numpy())
+        eng.close()
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
