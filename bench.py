@@ -64,6 +64,8 @@ def parse_args(argv=None):
     ap.add_argument("--cameras", type=int, default=0, help="PRNU cameras (default 64; 256 at C3)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--slots", type=int, default=0, help="home-only mode: device cache slots per GPU")
+    ap.add_argument("--home-only", action="store_true",
+                    help="force the C3 placement (items generated on their home GPU only) at any size")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--parity-samples", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
@@ -133,7 +135,8 @@ def workload(args, world):
 
 def home_only(args) -> bool:
     """C3-sized PCE jobs: patterns + spectra of all items do not fit one GPU."""
-    return args.app in ("pce", "ncc") and 2 * args.items * args.side * args.side * 4 > (120 << 30)
+    return args.app in ("pce", "ncc") and (getattr(args, "home_only", False) or
+                                           2 * args.items * args.side * args.side * 4 > (120 << 30))
 
 
 class ClockSampler:
