@@ -15,6 +15,7 @@
 // NCC runs as a tcgen05 Gram instead of per-pair launches: all items resident,
 // or key blocks of half the arena when the slots are fewer than the items.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -194,6 +195,39 @@ rk_status ledger_read(void* region, int64_t n, cudaStream_t s, rk_ledger_stats* 
   out->first_dup_pid = h[1] ? (int64_t)h[1] - 1 : -1;
   out->full = out->completed == total && out->dup_marks == 0;
   out->shared = 0;
+  return RK_OK;
+}
+
+// Peer-tier block copies over NVLink: the copy engine (cudaMemcpyAsync) or an
+// SM-driven copy (RK_PEER_COPY_CTAS > 0 CTAs of 512 threads, four 16-byte peer
+// loads in flight per thread through the IPC mapping, local stores).
+__global__ void __launch_bounds__(512) peer_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                        size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
+}
+
+int peer_copy_ctas() {
+  const char* v = getenv("RK_PEER_COPY_CTAS");
+  return v && *v ? atoi(v) : 0;
+}
+
+rk_status peer_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  const int ctas = peer_copy_ctas();
+  if (ctas > 0 && bytes % 16 == 0 && ((uintptr_t)dst | (uintptr_t)src) % 16 == 0) {
+    peer_copy_kernel<<<ctas, 512, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), bytes / 16);
+    RK_CUDA(cudaGetLastError());
+    return RK_OK;
+  }
+  RK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
   return RK_OK;
 }
 
@@ -582,15 +616,21 @@ rk_status ncc_blocked_run(rk_engine* e, const void* h_parsed, const void* d_pars
 rk_status ncc_peer_run(rk_engine* e, double* d_out, uint8_t* d_flags, int64_t launches0) {
   const int32_t n = e->app->p.n, w = e->p.world, r = e->p.rank;
   const int grp = std::max(1, e->app->slot_group);
-  const int32_t B = (int32_t)(e->arena_slots / 2) / grp * grp;
-  if (B < grp)
+  const int32_t Bmax = (int32_t)(e->arena_slots / 2) / grp * grp;
+  if (Bmax < grp)
     return set_error(RK_ERR_NO_EVICTABLE, "NCC over the peer tier needs >= %d device slots (have %zu)", 2 * grp,
                      e->arena_slots);
+  auto home_cnt = [&](int32_t s) { return n > s ? (n - s + w - 1) / w : 0; };
+  // an even number T of sub-blocks per rank (at least 2): with the (t, s) order the
+  // diametric block pairs then split evenly over the ranks
+  int32_t T = std::max<int32_t>(2, (home_cnt(0) + Bmax - 1) / Bmax);
+  T += T & 1;
+  const int32_t tile = grp * 2;   // 256-item Gram tiles
+  const int32_t B = std::min(Bmax, std::max(grp, ((home_cnt(0) + T - 1) / T + tile - 1) / tile * tile));
   struct Sub {
     int32_t s, m0, cnt;
   };
   std::vector<Sub> subs;
-  auto home_cnt = [&](int32_t s) { return n > s ? (n - s + w - 1) / w : 0; };
   int32_t tmax = 0;
   for (int32_t s = 0; s < w; ++s) tmax = std::max(tmax, (home_cnt(s) + B - 1) / B);
   for (int32_t t = 0; t < tmax; ++t)
@@ -653,9 +693,8 @@ rk_status ncc_peer_run(rk_engine* e, double* d_out, uint8_t* d_flags, int64_t la
       // whole slot groups: the NCC layout interleaves each group's 128 items ([D/1024][128][1024]),
       // so a partial group is not a byte prefix (home regions are allocated in whole groups)
       const size_t rows = (size_t)(subs[b].cnt + grp - 1) / grp * grp;
-      RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + (size_t)f * B * stride,
-                              e->peer_home[subs[b].s] + (size_t)subs[b].m0 * stride, rows * stride,
-                              cudaMemcpyDeviceToDevice, e->lstream));
+      RK_TRY(peer_copy(static_cast<char*>(e->arena) + (size_t)f * B * stride,
+                       e->peer_home[subs[b].s] + (size_t)subs[b].m0 * stride, rows * stride, e->lstream));
       trace_end(e, tk, e->lstream);
       RK_CUDA(cudaEventRecord(ev_fetched[f], e->lstream));
       for (int q = 0; q < S; ++q) RK_CUDA(cudaStreamWaitEvent(e->gstreams[q], ev_fetched[f], 0));
@@ -1264,10 +1303,15 @@ rk_status rk_engine_peer_bandwidth(rk_engine* e, int32_t src_rank, size_t bytes,
   RK_CUDA(cudaEventCreate(&a));
   RK_CUDA(cudaEventCreate(&b));
   RK_CUDA(cudaEventRecord(a, e->lstream));
-  // the same copy the run issues for a peer fetch, in slot-sized pieces
-  for (size_t off = 0; off < bytes; off += e->slot_stride)
-    RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + off, e->peer_home[src_rank] + off,
-                            std::min(e->slot_stride, bytes - off), cudaMemcpyDeviceToDevice, e->lstream));
+  // the copies the run issues: slot-sized pieces (PCE / CV / GMM peer fetches), or
+  // one block (the NCC Gram's sub-block fetch) when the app is NCC
+  if (e->app->p.kind == RK_APP_NCC) {
+    RK_TRY(peer_copy(e->arena, e->peer_home[src_rank], bytes, e->lstream));
+  } else {
+    for (size_t off = 0; off < bytes; off += e->slot_stride)
+      RK_CUDA(cudaMemcpyAsync(static_cast<char*>(e->arena) + off, e->peer_home[src_rank] + off,
+                              std::min(e->slot_stride, bytes - off), cudaMemcpyDeviceToDevice, e->lstream));
+  }
   RK_CUDA(cudaEventRecord(b, e->lstream));
   RK_CUDA(cudaEventSynchronize(b));
   float ms = 0.f;
