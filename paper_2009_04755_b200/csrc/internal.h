@@ -137,7 +137,6 @@ struct PceState {
   float2* T = nullptr;     // clusters * t_stride: column-pass output, one slot per cluster
   size_t t_stride = 0;     // float2 between T slots: (N/2)*N + padding (breaks the power-of-two stride)
   PairJob* job = nullptr;   // host staging of the launch parameters
-  CUtensorMap tmap_T;       // T as [cluster][8-row block][column][64 B] for the TMA column stores
 };
 
 struct CvState {};

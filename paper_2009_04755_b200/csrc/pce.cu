@@ -28,8 +28,10 @@
 //   reduction     fixed-order combine of the warp partials (deterministic)
 //   window        6 warps recompute the 11 rows around the peak from staged
 //                 blocks and sum the 11x11 energy; one thread writes PCE + flag.
-// CL > 1 (a cluster per pair, DSMEM reductions, T kept in L2) is still
-// compilable for the measurements recorded below and in DESIGN.md.
+// 256^2 runs the same kernel with a cluster of 2 CTAs per pair (DSMEM
+// reductions); the measured-and-rejected variants of round 1 (clusters per pair at
+// 1024^2, TMA tensor stores of T, a padded transpose, group-slice column staging,
+// two 4-warp CTAs per SM, L2 policies) are recorded in DESIGN.md, not kept here.
 
 #include <math.h>
 #include <stdio.h>
@@ -49,52 +51,22 @@ using namespace pcek;
 constexpr int kGroups = 8;              // FFT groups (row-pairs / columns) per preprocess CTA
 constexpr int kRows = 2 * kGroups;      // rows per preprocess row-pass CTA
 constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] tile
-// warps per compare CTA: 8 lane groups (one per row pair of a 16-row block); one CTA per SM
-// Warp groups (4 lane groups each) per compare CTA: 2 (default: one CTA of 8 warps
-// per SM) or 1 (-DPCE_GROUPS=1: two independent 4-warp CTAs per SM, each on its own pair).
-#ifndef PCE_GROUPS
-#define PCE_GROUPS 2
-#endif
-__host__ __device__ constexpr int cta_warps(int R) { return 4 * PCE_GROUPS / (32 / R); }
-
-// Transpose buffer of the compare kernel: XOR-swizzled R*R (default) or padded
-// R*(R+1) for R = 32 (no per-element address registers; -DPCE_PAD_XPOSE=1).
-// Column-phase staging: per-warp slices and mbarriers (1) or one slice per warp
-// group refilled after a group barrier (0).
-#ifndef PCE_WARP_COLS
-#define PCE_WARP_COLS 1
-#endif
-
-// Column-phase T stores (R = 32): the warp stages its column's 128 T segments
-// (8 KiB) in its transpose buffer and one lane issues a single TMA tensor store
-// (1), or every lane stores its 32 values with STG (0, default: the TMA form
-// measured 408k vs 418k pairs/s, same box, at a 20 MHz lower power-capped clock).
-#ifndef PCE_TMA_STORE
-#define PCE_TMA_STORE 0
-#endif
-
-#ifndef PCE_PAD_XPOSE
-#define PCE_PAD_XPOSE 0
-#endif
-__host__ __device__ constexpr int xpose_size(int R) { return (PCE_PAD_XPOSE && R == 32) ? R * (R + 1) : R * R; }
+// Warps per compare CTA: two independent warp groups of 4 lane groups each
+// (8 warps at R = 32, 4 warps of two half-warp lane groups at R = 16).
+__host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
+__host__ __device__ constexpr int xpose_size(int R) { return R * R; }   // XOR-swizzled transpose buffer
 template <int R>
 __device__ __forceinline__ void compare_fft(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
-  if constexpr (PCE_PAD_XPOSE && R == 32) group_fft_pad_rt<R, true>(v, xbuf, w, lane);
-  else group_fft_rt<R, true>(v, xbuf, w, lane);
+  group_fft_rt<R, true>(v, xbuf, w, lane);
 }
 
+// CTAs per pair: 1 at R = 32 (one SM per pair in flight, all 148 SMs; clusters of
+// 2 / 4 / 8 measured slower), 2 at R = 16.
 template <int R>
 struct ClusterShape;
-#ifndef PCE_CL
-#define PCE_CL 1
-#endif
-// Measured on B200 (N = 1024 bench, 1024-pair launches): CL = 8 keeps every T
-// slot L2-resident but only 15 clusters (120 SMs) fit and the per-pair cluster
-// barriers dominate (277k pairs/s); CL = 4: 314k; CL = 2: 376k; CL = 1 (one SM
-// per pair, all 148 SMs, T round-trips through HBM): 383k pairs/s.
 template <>
 struct ClusterShape<32> {
-  static constexpr int CL = PCE_CL;
+  static constexpr int CL = 1;
 };
 template <>
 struct ClusterShape<16> {
@@ -229,29 +201,16 @@ __device__ unsigned long long g_pce_probe[148 * 2 * 8];
   } while (0)
 #endif
 
-// TMA tensor store of one staged column of T (bulk group of the issuing thread).
-__device__ __forceinline__ void tma_store_col(const CUtensorMap* map, const void* src, int col, int cid) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
-               ::"l"(map), "r"(0), "r"(col), "r"(0), "r"(cid), "r"(smem_u32(src)) : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// the source buffers of this thread's bulk stores may be overwritten
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-// this thread's bulk stores are complete (visible in global memory)
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 template <int R, int CL>
-__global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster(
+__global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
-    const __grid_constant__ CUtensorMap tmap_T, const LedgerRef ledger) {
+    const LedgerRef ledger) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
-  constexpr bool kTmaStore = PCE_TMA_STORE && R == 32;
   constexpr int kCtaWarps = cta_warps(R);
   constexpr int NT = kCtaWarps * 32;
-  constexpr int kNG = PCE_GROUPS;         // independent warp groups
+  constexpr int kNG = 2;                  // independent warp groups
   constexpr int kGW = kCtaWarps / kNG;    // warps per warp group
   constexpr int kGL = kGW * G;            // lane groups per warp group: 4 columns / 4 row pairs per round
   constexpr int NCOL = (N / 2) / CL;      // columns per CTA
@@ -267,7 +226,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
   float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
   __shared__ __align__(8) uint64_t s_bar[kNG][3];   // per group: column slices, row block 0 / 1
   __shared__ __align__(8) uint64_t s_wbar;
-  __shared__ __align__(8) uint64_t s_cbar[kCtaWarps];   // per warp: its column slice (PCE_WARP_COLS)
+  __shared__ __align__(8) uint64_t s_cbar[kCtaWarps];   // per warp: its column slice
   __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
   __shared__ float s_wpart[8];            // window energy per row pair, gathered in CTA 0
   __shared__ float s_v[kCtaWarps];
@@ -298,27 +257,20 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
   }
   uint32_t ph = 0;                        // parity bits of this group's three barriers (bit b)
   uint32_t wph = 0;
-  uint32_t cph = 0;                       // parity of this warp's column-slice barrier (PCE_WARP_COLS)
+  uint32_t cph = 0;                       // parity of this warp's column-slice barrier
   __syncthreads();
   const uint32_t part0 = dsmem_addr(&s_part[0], 0);
   const uint32_t wpart0 = dsmem_addr(&s_wpart[0], 0);
   float2 twr[R];   // this lane's twiddles W_N^(lane*k1): no shared-memory traffic in the FFTs
 #pragma unroll
   for (int k1 = 0; k1 < R; ++k1) twr[k1] = tw[k1 * R + lane];
-#ifndef PCE_T_POLICY
-#define PCE_T_POLICY 2
-#endif
-#ifndef PCE_SPEC_POLICY
-#define PCE_SPEC_POLICY 2
-#endif
-  // L2 priority (0 = evict_last, 1 = evict_first, 2 = evict_normal).  With one pair
-  // per SM (148 T slots, 592 MiB) T cannot stay in L2, so neither T nor the spectra
-  // (reused by the neighbouring pairs of a leaf) get a special priority.
+  // L2 priority: with one pair per SM (148 T slots, 592 MiB) T cannot stay in L2,
+  // so neither T nor the spectra (reused by the neighbouring pairs of a leaf) get a
+  // special priority (evict_last / evict_first measured within 1 %); T blocks are
+  // read once, evict_first.
   const uint64_t pol_first = l2_policy_evict_first();
-  const uint64_t pol_T = PCE_T_POLICY == 0 ? l2_policy_evict_last()
-                         : PCE_T_POLICY == 1 ? pol_first : l2_policy_evict_normal();
-  const uint64_t pol_spec = PCE_SPEC_POLICY == 0 ? l2_policy_evict_last()
-                            : PCE_SPEC_POLICY == 1 ? pol_first : l2_policy_evict_normal();
+  const uint64_t pol_T = l2_policy_evict_normal();
+  const uint64_t pol_spec = pol_T;
   cluster_sync();
 
   for (int pi = cid; pi < job.npairs; pi += ncl) {
@@ -335,7 +287,6 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
     {
       const int cbeg = q * NCOL + 4 * wg, cend = (q + 1) * NCOL;
-#if PCE_WARP_COLS
       // Per-warp pipeline: each warp owns the G columns of X and Y its lane groups
       // transform, waits on its own mbarrier and refills its own slice as soon as its
       // products are in registers -- no group barrier couples the four warps.
@@ -356,22 +307,6 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
         cph ^= 1u;
         const float2* X = gb + gi * N;
         const float2* Y = gb + kHalf + gi * N;
-#else
-      uint64_t* bar = &s_bar[wg][0];
-      if (leader) {
-        refill_fence();
-        mbar_expect_tx(bar, 2 * kHalfBytes);
-        bulk_g2s_hint(gb, Xs + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
-        bulk_g2s_hint(gb + kHalf, Ys + (size_t)cbeg * N, kHalfBytes, bar, pol_spec);
-      }
-#pragma unroll 1
-      for (int c0 = cbeg; c0 < cend; c0 += 4 * kNG) {
-        const int col = c0 + gi;
-        mbar_wait(bar, ph & 1u);
-        ph ^= 1u;
-        const float2* X = gb + gi * N;
-        const float2* Y = gb + kHalf + gi * N;
-#endif
         if (col != 0) {
 #pragma unroll
           for (int n2 = 0; n2 < R; ++n2) v[n2] = c_mulc(X[lane + R * n2], Y[lane + R * n2]);
@@ -395,7 +330,6 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
             v[n2] = make_float2(pa.x - pb.y, pa.y + pb.x);
           }
         }
-#if PCE_WARP_COLS
         __syncwarp();                  // this warp's columns are consumed
         if (wl == 0 && c0 + 4 * kNG < cend) {
           refill_fence();
@@ -403,42 +337,14 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 2 / PCE_GROUPS) pce_cluster
           bulk_g2s_hint(wx, Xs + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);
           bulk_g2s_hint(wy, Ys + (size_t)(c0 + 4 * kNG + wcol) * N, kWarpBytes, wbar, pol_spec);
         }
-#else
-        named_bar(1 + wg, kGW * 32);   // this group's slices are consumed
-        if (leader && c0 + 4 * kNG < cend) {
-          refill_fence();
-          mbar_expect_tx(bar, 2 * kHalfBytes);
-          bulk_g2s_hint(gb, Xs + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
-          bulk_g2s_hint(gb + kHalf, Ys + (size_t)(c0 + 4 * kNG) * N, kHalfBytes, bar, pol_spec);
-        }
-#endif
-        if (kTmaStore) {   // the previous column's store has read the transpose buffer
-          if (wl == 0) bulk_wait_read();
-          __syncwarp();
-        }
         compare_fft<R>(v, xbuf, twr, lane);
         // row lane + R*k2 -> 8-row block (lane>>3) + (R/8)*k2, row lane&7 (chunk-swizzled)
         const int rr = lane & 7;
         const int pos = (((rr >> 1) ^ ((col >> 1) & 3)) << 1) | (rr & 1);
-        if (kTmaStore) {
-          // stage the column as T's 128 segments of 64 B ([block][8 rows], swizzled) in the
-          // (free) transpose buffer, then one tensor store writes all of them
-          float2* stg = xbuf + (lane >> 3) * 8 + pos;
+        float2* dst = Tp + ((size_t)(lane >> 3) * (N / 2) + col) * 8 + pos;
+        constexpr size_t kStep = (size_t)(R / 8) * (N / 2) * 8;
 #pragma unroll
-          for (int k2 = 0; k2 < R; ++k2) stg[k2 * (R / 8) * 8] = v[k2];
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (wl == 0) tma_store_col(&tmap_T, xbuf, col, cid);
-        } else {
-          float2* dst = Tp + ((size_t)(lane >> 3) * (N / 2) + col) * 8 + pos;
-          constexpr size_t kStep = (size_t)(R / 8) * (N / 2) * 8;
-#pragma unroll
-          for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
-        }
-      }
-      if (kTmaStore) {   // T complete in global memory before the barrier; buffer reusable
-        if (wl == 0) bulk_wait_all();
-        __syncwarp();
+        for (int k2 = 0; k2 < R; ++k2) stg_hint(dst + k2 * kStep, v[k2], pol_T);
       }
     }
     PCE_PROBE(1);
@@ -595,7 +501,7 @@ template <int R>
 size_t cluster_smem() {
   constexpr int N = R * R;
   // 2 warp groups x 2 x 4N (column slices / 8-row blocks) + twiddles + one transpose per lane group
-  return (size_t)(8 * PCE_GROUPS * N + R * R + cta_warps(R) * (32 / R) * xpose_size(R)) * sizeof(float2);
+  return (size_t)(16 * N + R * R + cta_warps(R) * (32 / R) * xpose_size(R)) * sizeof(float2);
 }
 
 template <int R>
@@ -660,7 +566,7 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
   RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, st.t_stride, (const float2*)st.tw, d_out,
-                             d_flags, threshold_or_nan(app), st.tmap_T, app->ledger));
+                             d_flags, threshold_or_nan(app), app->ledger));
   app->launches += 1;
   return RK_OK;
 }
@@ -678,20 +584,6 @@ rk_status cluster_init(rk_app* app) {
   st.clusters = clusters;
   st.t_stride = (size_t)(N / 2) * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * clusters));
-  memset(&st.tmap_T, 0, sizeof(st.tmap_T));
-  if (PCE_TMA_STORE && R == 32) {
-    // [cluster][8-row block][column][8 rows x complex64 = 16 floats]; box = one column
-    EncodeTiledFn encode = nullptr;
-    RK_TRY(tensor_map_encoder(&encode));
-    const cuuint64_t dims[4] = {16, (cuuint64_t)(N / 2), (cuuint64_t)(N / 8), (cuuint64_t)clusters};
-    const cuuint64_t strides[3] = {64, (cuuint64_t)(N / 2) * 64, (cuuint64_t)st.t_stride * sizeof(float2)};
-    const cuuint32_t box[4] = {16, 1, (cuuint32_t)(N / 8), 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult cr = encode(&st.tmap_T, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, st.T, dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return set_error(RK_ERR_DEVICE, "cuTensorMapEncodeTiled (PCE T) failed (%d)", (int)cr);
-  }
   st.job = new PairJob();
   return RK_OK;
 }
