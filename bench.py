@@ -292,6 +292,10 @@ def _worker_step(count):
 class CpuArm:
     """The oracle port on every host core (one pinned process per core)."""
 
+    @staticmethod
+    def host_cores() -> int:
+        return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
     def __init__(self, args, step_seconds: float):
         import multiprocessing as mp
         import random
@@ -363,6 +367,77 @@ def cpu_baseline(args, budget_s):
             "sample": arm.describe(cpu_what(args)) + f"; 3 steps, {done} compares in {wall:.1f}s"}
 
 
+def realengine_sample(args, n_items=16, lanes=1):
+    """BASELINE.md section 3's harness: the reference's own RealEngine
+    (realrun.py:28-176, staged in oracle/_ref by oracle/Makefile) running a float64
+    numpy Application (oracle/pce.py, or oracle/ncc.py) over n_items of this
+    workload: real mode, one node, `lanes` device lanes, cpu_width = host cores,
+    stage_cost = 0.  Returns pairs/s of the whole run (load stage included)."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "allpairs")):
+        return {"unavailable": "oracle/_ref not staged (make -C oracle where /root/reference exists)"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import struct
+
+    import numpy as np
+    from allpairs.apps import Application, ItemData, PairResult, Stage
+    from allpairs.config import NodeShape, RunConfig
+    from allpairs.realrun import RealEngine
+
+    from oracle import ncc as oncc
+    from oracle import pce as opce
+    side, ncc = args.side, args.app == "ncc"
+
+    class NumpyApp(Application):
+        name = "numpy-" + ("ncc" if ncc else "pce")
+
+        def path_for_key(self, key):
+            return f"prnu/{key:06d}.f32"
+
+        def fetch_raw(self, path):
+            return opce.prnu_patterns(side, side, int(path[5:11]), 1, args.cameras, args.seed)[0].tobytes()
+
+        def parse(self, key, raw):
+            return ItemData(Stage.PARSED, raw.payload)
+
+        def preprocess(self, key, parsed):
+            x = np.frombuffer(parsed.payload, dtype=np.float32).reshape(side, side)
+            y = oncc.preprocess(x) if ncc else opce.preprocess(x)
+            return ItemData(Stage.PREPROCESSED, y.tobytes(), sim_bytes=self.slot_size)
+
+        def compare(self, left, right):
+            (i, a), (j, b) = left, right
+            if ncc:
+                v = oncc.compare(np.frombuffer(a.payload), np.frombuffer(b.payload))
+            else:
+                sa = np.frombuffer(a.payload, dtype=np.complex128).reshape(side, side // 2 + 1)
+                sb = np.frombuffer(b.payload, dtype=np.complex128).reshape(side, side // 2 + 1)
+                v = opce.compare(sa, sb, side, side)
+            return struct.pack("<d", v)
+
+        def postprocess(self, pair, raw):
+            (v,) = struct.unpack("<d", raw)
+            return PairResult(pair[0], pair[1], v, match=v >= (0.02 if ncc else 60.0))
+
+        def stage_cost(self, stage, i, j=None):
+            return 0.0
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    app = NumpyApp(n_items, slot_size=side * (side // 2 + 1) * 16)
+    cfg = RunConfig(app={"kind": app.name}, mode="real", leaf_block=args.leaf,
+                    nodes=[NodeShape(device_speeds=[1.0] * lanes, device_slots=n_items, host_slots=n_items,
+                                     cpu_width=cores)])
+    t0 = time.perf_counter()
+    master = RealEngine(cfg, app, run_timeout=600).run()
+    wall = time.perf_counter() - t0
+    pairs = n_items * (n_items - 1) // 2
+    return {"value": pairs / wall, "unit": "pairs/s", "pairs": pairs, "seconds": wall, "device_lanes": lanes,
+            "cpu_width": cores, "ledger_full": bool(master.ledger.full),
+            "what": f"reference RealEngine (oracle/_ref) + float64 numpy app, {n_items} items of {side}^2, "
+                    "real mode, one node, load stage included"}
+
+
 def reference_arm(args, world_env, rank):
     """`--impl reference`: the reference-side CPU path, timed like our arm (W + K steps)."""
     if rank != 0:
@@ -379,6 +454,15 @@ def reference_arm(args, world_env, rank):
         step_ms.append(w * 1e3)
     arm.close()
     value = done / wall
+    harness = None
+    if args.app in ("pce", "ncc") and not args.no_cpu:
+        # the reference's own engine on a bounded sample, one and
+        # all device lanes; a reported figure beside the value, which is the (faster) port
+        n_re = 16 if args.side >= 1024 else min(args.items, 32)
+        try:
+            harness = [realengine_sample(args, n_re, lanes) for lanes in (1, CpuArm.host_cores())]
+        except Exception as exc:   # the arm's value stands without it
+            harness = {"error": str(exc)[:200]}
     line = {"metric": metric, "value": value, "unit": "pairs/s", "impl": "reference", "n_gpus": args.gpus,
             "host_only": True, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -386,7 +470,8 @@ def reference_arm(args, world_env, rank):
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": arm.cores, "kind": "port",
                              "sample": arm.describe(cpu_what(args)),
                              "pairs_per_step": done // max(1, args.steps), "step_ms": step_ms},
-            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "realengine": harness}
     print(json.dumps(line), flush=True)
     return 0
 
