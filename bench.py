@@ -1062,7 +1062,11 @@ def main_app(args, rank, world, local_rank):
     ledger = eng.ledger() if rank == 0 else None
     e2e = None
     parsed_total = n * stride
-    if not args.no_e2e and parsed_total <= (24 << 30):
+    try:   # pinned host copy of every parsed item: at most a third of the host's memory
+        host_ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError, AttributeError):
+        host_ram = 64 << 30
+    if not args.no_e2e and parsed_total <= host_ram // 3:
         host = torch.empty(parsed_total, dtype=torch.uint8, pin_memory=True)
         host.copy_(items)
         res_host = torch.empty(pairs_total, dtype=torch.float64, pin_memory=True)
