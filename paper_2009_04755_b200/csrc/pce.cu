@@ -54,18 +54,10 @@ constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] til
 // Warps per compare CTA: two independent warp groups of 4 lane groups each
 // (8 warps at R = 32, 4 warps of two half-warp lane groups at R = 16).
 __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
-// Transpose buffer per lane group: padded to a stride of R + 1 float2 (1, default)
-// so every transpose address is the lane's base plus a compile-time offset, or
-// the XOR-swizzled R x R layout (0) whose per-element address arithmetic was
-// ~120k LOP3/IADD3/LEA per pair (11 % of the kernel's instructions, ncu r2).
-#ifndef PCE_XPOSE_PAD
-#define PCE_XPOSE_PAD 1
-#endif
-__host__ __device__ constexpr int xpose_size(int R) { return PCE_XPOSE_PAD ? R * (R + 1) : R * R; }
+__host__ __device__ constexpr int xpose_size(int R) { return R * R; }   // XOR-swizzled transpose buffer
 template <int R>
 __device__ __forceinline__ void compare_fft(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
-  if constexpr (PCE_XPOSE_PAD) group_fft_pad_rt<R, true>(v, xbuf, w, lane);
-  else group_fft_rt<R, true>(v, xbuf, w, lane);
+  group_fft_rt<R, true>(v, xbuf, w, lane);
 }
 
 // CTAs per pair: 1 at R = 32 (one SM per pair in flight, all 148 SMs; clusters of
