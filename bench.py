@@ -729,9 +729,13 @@ def main_pce(args, rank, world, local_rank):
     torch.cuda.synchronize()
     state = {"connected": False}
 
+    load_ms = []
+
     def load_home_streamed():
         # the load stage of home-only mode: generate (storage) + preprocess, 256 items at a time
         home = list(range(rank, n, world))
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(estream)
         with torch.cuda.stream(estream):
             for m0 in range(0, len(home), 256):
                 cnt = min(256, len(home) - m0)
@@ -739,6 +743,9 @@ def main_pce(args, rank, world, local_rank):
                     device.synth_prnu(side, side, home[m0 + q], 1, args.cameras, args.seed,
                                       gen.narrow(0, q * ss, ss), stream=estream)
                 eng.load_home_range(m0, cnt, device_items=gen, parsed_stride=parsed_bytes)
+        h1.record(estream)
+        h1.synchronize()
+        load_ms.append(h0.elapsed_time(h1))
 
     def step(host_home=None, host_all=None):
         """One full job on this rank: [home preprocess + barrier] + all of its pairs [+ barrier]."""
@@ -779,6 +786,7 @@ def main_pce(args, rank, world, local_rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(estream)
     kms, ksamples, kpairs = 0.0, 0, 0
+    load_ms.clear()
     for _ in range(args.steps):
         step()
         a, b, c = eng.kernel_time()
@@ -801,6 +809,16 @@ def main_pce(args, rank, world, local_rank):
     else:
         all_pairs = float(my_pairs)
     value = all_pairs / (ms / 1e3)
+    breakdown = None
+    if streamed:
+        # per job: the home load stage (generation = the storage read, + preprocess) and the
+        # rest (barrier, all pairs, barrier), max over ranks
+        lt = torch.tensor([sum(load_ms) / max(1, len(load_ms))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+        breakdown = {"home_load_ms": float(lt[0]), "pairs_ms": ms / args.steps - float(lt[0]),
+                     "what": "home_load = synthetic generation (the storage read) + preprocess of this rank's "
+                             "home items; pairs = the rest of the job (max over ranks)"}
     eng.set_profiling(0)
     # cache accounting over the whole job (runner.py:41 R = loads / n; slotcache.py:252-260 tiers)
     ct = torch.tensor([st["loads"], st["hits"], st["misses"], st["peer_fetches"], st["steals"],
@@ -963,7 +981,7 @@ def main_pce(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": cfg,
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "parity": parity,
-            "perf_model": perf, "gpu_launches": st["kernel_launches"],
+            "perf_model": perf, "job_breakdown": breakdown, "gpu_launches": st["kernel_launches"],
             "ledger": dict(ledger, what="device bitmap of C(n,2) bits set by every compare epilogue "
                                         "(atomicOr over NVLink into rank 0's ledger at N > 1), last timed job"),
             "cache": {"R": loads_all / n, "loads_per_step": loads_all, "device_slots_per_gpu": dslots,
