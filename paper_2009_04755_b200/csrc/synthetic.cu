@@ -2,6 +2,8 @@
 // deterministic PRNU-like pattern generator used for synthetic workloads.
 #include <math.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace rk {
@@ -66,16 +68,29 @@ __device__ __forceinline__ float normal_from_hash(uint64_t h) {
 
 constexpr float kPrnuGain = 0.2f;  // PRNU amplitude relative to unit-variance noise
 
-__global__ void synth_prnu_kernel(int64_t hw, int32_t first_key, int32_t n_items, int32_t cameras, uint64_t seed,
-                                  float* __restrict__ out) {
-  const int64_t total = hw * n_items;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = t / hw, pix = t % hw;
-    const int64_t key = first_key + item;
-    const int64_t cam = key % cameras;
-    const float k = normal_from_hash(mix64_4(seed, 0x50524E55ull, (uint64_t)cam, (uint64_t)pix));
-    const float e = normal_from_hash(mix64_4(seed, 0x4E4F4953ull, (uint64_t)key, (uint64_t)pix));
-    out[t] = fmaf(kPrnuGain, k, e);
+// One CTA row (blockIdx.y) per item: the key / camera are per-thread constants
+// (no 64-bit division per element); four consecutive pixels per thread, one
+// float4 store.  The values are those of the scalar definition bit for bit.
+__global__ void __launch_bounds__(256) synth_prnu_kernel(int64_t hw, int32_t first_key, int32_t cameras,
+                                                         uint64_t seed, float* __restrict__ out) {
+  const int64_t key = first_key + (int64_t)blockIdx.y;
+  const uint64_t cam = (uint64_t)(key % cameras);
+  float* o = out + (int64_t)blockIdx.y * hw;
+  for (int64_t p4 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; p4 < hw;
+       p4 += (int64_t)gridDim.x * blockDim.x * 4) {
+    float r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t pix = (uint64_t)(p4 + q);
+      const float k = normal_from_hash(mix64_4(seed, 0x50524E55ull, cam, pix));
+      const float e = normal_from_hash(mix64_4(seed, 0x4E4F4953ull, (uint64_t)key, pix));
+      r[q] = fmaf(kPrnuGain, k, e);
+    }
+    if (p4 + 3 < hw) {
+      *reinterpret_cast<float4*>(o + p4) = make_float4(r[0], r[1], r[2], r[3]);
+    } else {
+      for (int q = 0; q < 4 && p4 + q < hw; ++q) o[p4 + q] = r[q];
+    }
   }
 }
 
@@ -103,10 +118,16 @@ rk_status synth_tile(rk_app* app, int32_t r0, int32_t r1, int32_t c0, int32_t c1
 
 rk_status synth_prnu(int32_t h, int32_t w, int32_t first_key, int32_t n_items, int32_t cameras, uint64_t seed,
                      float* d_out, cudaStream_t s) {
-  const int64_t total = (int64_t)h * w * n_items;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  synth_prnu_kernel<<<blocks, 256, 0, s>>>((int64_t)h * w, first_key, n_items, cameras, seed, d_out);
+  const int64_t hw = (int64_t)h * w;
+  if (n_items <= 0 || hw <= 0) return RK_OK;
+  if (((uintptr_t)d_out & 15) != 0 || hw % 4 != 0)
+    return set_error(RK_ERR_VALUE, "synthetic patterns: 16-byte aligned output and h*w % 4 == 0 required");
+  int bx = (int)std::min<int64_t>((hw / 4 + 255) / 256, std::max<int64_t>(1, 148 * 8 / std::max(1, n_items)));
+  bx = std::max(bx, 1);
+  for (int32_t i0 = 0; i0 < n_items; i0 += 65535) {
+    const int32_t m = std::min(65535, n_items - i0);
+    synth_prnu_kernel<<<dim3(bx, m), 256, 0, s>>>(hw, first_key + i0, cameras, seed, d_out + (int64_t)i0 * hw);
+  }
   RK_CUDA(cudaGetLastError());
   return RK_OK;
 }

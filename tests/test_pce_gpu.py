@@ -369,3 +369,19 @@ def test_compare_is_deterministic_run_to_run(side, n, runs):
         eng.close()
     for o in outs[1:]:
         np.testing.assert_array_equal(o, outs[0])
+
+
+def test_synthetic_patterns_match_the_oracle_generator():
+    """rk_synth_prnu (the bench's storage stage) against its float64 restatement
+    (oracle/pce.py prnu_patterns) to fp32 rounding, and bit-identical whether items
+    are generated in one call or one at a time at any key offset."""
+    _l, device = _lib()
+    side, n = 256, 5
+    one = make_items(n, side, cameras=3, seed=7)
+    each = torch.empty_like(one)
+    for k in range(n):
+        device.synth_prnu(side, side, k, 1, 3, 7, each[k * side * side:(k + 1) * side * side])
+    torch.cuda.synchronize()
+    assert torch.equal(one, each)
+    want = opce.prnu_patterns(side, side, 0, n, 3, 7)
+    np.testing.assert_allclose(one.cpu().numpy().reshape(n, side, side), want, rtol=1e-4, atol=1e-4)
