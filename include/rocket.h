@@ -315,6 +315,12 @@ rk_status rk_tier_release(rk_tier* tier, int32_t slot);
 /* out5 = {hits, misses, waits, evictions, occupancy} (snapshot_stats, slotcache.py:252-260) */
 rk_status rk_tier_stats(const rk_tier* tier, int64_t* out5);
 int32_t rk_tier_slot_key(const rk_tier* tier, int32_t slot);
+/* One work-queue transition on a word value (head << 32 | tail): op 0 = the owner
+ * takes up to `arg` leaves from the head, op 1 = a thief takes the back half when
+ * at least `arg` leaves remain on each side.  Returns 1 with the new word and the
+ * taken range (same encoding), 0 when nothing can be taken, -1 on bad arguments.
+ * The device queue applies exactly this transition under atomicCAS_system. */
+int32_t rk_queue_step(uint64_t old_word, int32_t op, uint64_t arg, uint64_t* new_word, uint64_t* taken);
 /* Depth-first quadtree leaves (iter_leaves, scheduler.py:78-86) of this rank's
  * share; writes min(count, cap) leaves as (r0, r1, c0, c1) and returns count. */
 int64_t rk_leaves(int32_t n, int32_t leaf_block, int32_t rank, int32_t world, int32_t* out4, int64_t cap);

@@ -172,6 +172,7 @@ SIGNATURES = [
     ("rk_tier_release", C.c_int, [C.c_void_p, C.c_int32]),
     ("rk_tier_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     ("rk_tier_slot_key", C.c_int32, [C.c_void_p, C.c_int32]),
+    ("rk_queue_step", C.c_int32, [C.c_uint64, C.c_int32, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("rk_leaves", C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int64]),
 ]
 

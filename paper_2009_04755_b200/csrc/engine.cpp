@@ -110,6 +110,28 @@ std::pair<int, int> rank_range(const std::vector<Leaf>& leaves, int rank, int wo
 // the front) and publishes it as its own range, so it can be re-stolen.  The
 // words live in device memory and peers update them with system-scope atomics
 // over NVLink (CUDA IPC mappings); the host reads the result from mapped memory.
+// One queue transition on a word value: op 0 = the owner takes up to `arg` leaves
+// from the head, op 1 = a thief takes the back half if at least `arg` leaves
+// remain on each side.  False when there is nothing to take.  Shared by the device
+// CAS loop and the host test hook rk_queue_step.
+__host__ __device__ inline bool queue_step(unsigned long long old, int op, unsigned long long arg,
+                                           unsigned long long* nw, unsigned long long* got) {
+  const unsigned h = (unsigned)(old >> 32), t = (unsigned)old;
+  const unsigned rem = t > h ? t - h : 0u;
+  if (op == 0) {
+    if (rem == 0) return false;
+    const unsigned take = rem < arg ? rem : (unsigned)arg;
+    *nw = ((unsigned long long)(h + take) << 32) | t;
+    *got = ((unsigned long long)h << 32) | (h + take);
+    return true;
+  }
+  if (rem < 2 * arg) return false;
+  const unsigned k = rem / 2;
+  *nw = ((unsigned long long)h << 32) | (t - k);
+  *got = ((unsigned long long)(t - k) << 32) | t;
+  return true;
+}
+
 __global__ void queue_op_kernel(unsigned long long* word, int op, unsigned long long arg,
                                 unsigned long long* res) {
   unsigned long long old = atomicAdd_system(word, 0ull);
@@ -123,25 +145,10 @@ __global__ void queue_op_kernel(unsigned long long* word, int op, unsigned long 
     return;
   }
   for (;;) {
-    const unsigned h = (unsigned)(old >> 32), t = (unsigned)old;
-    const unsigned rem = t > h ? t - h : 0u;
     unsigned long long nw, got;
-    if (op == 0) {          // owner: up to `arg` leaves from the head
-      if (rem == 0) {
-        *res = ~0ull;
-        return;
-      }
-      const unsigned take = rem < arg ? rem : (unsigned)arg;
-      nw = ((unsigned long long)(h + take) << 32) | t;
-      got = ((unsigned long long)h << 32) | (h + take);
-    } else {                // thief: the back half, if at least `arg` leaves remain on each side
-      if (rem < 2 * arg) {
-        *res = ~0ull;
-        return;
-      }
-      const unsigned k = rem / 2;
-      nw = ((unsigned long long)h << 32) | (t - k);
-      got = ((unsigned long long)(t - k) << 32) | t;
+    if (!queue_step(old, op, arg, &nw, &got)) {
+      *res = ~0ull;
+      return;
     }
     const unsigned long long prev = atomicCAS_system(word, old, nw);
     if (prev == old) {
@@ -1448,6 +1455,15 @@ rk_status rk_tier_stats(const rk_tier* t, int64_t* out5) {
 int32_t rk_tier_slot_key(const rk_tier* t, int32_t slot) {
   if (!t || slot < 0 || slot >= t->t.capacity) return -1;
   return t->t.key[slot];
+}
+
+int32_t rk_queue_step(uint64_t old, int32_t op, uint64_t arg, uint64_t* nw, uint64_t* got) {
+  if (!nw || !got || op < 0 || op > 1) return -1;
+  unsigned long long a = 0, b = 0;
+  if (!queue_step(old, op, arg, &a, &b)) return 0;
+  *nw = a;
+  *got = b;
+  return 1;
 }
 
 int64_t rk_leaves(int32_t n, int32_t leaf_block, int32_t rank, int32_t world, int32_t* out4, int64_t cap) {
