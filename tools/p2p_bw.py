@@ -22,6 +22,20 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 
+def nvlink_counters(gpu: int):
+    """Summed NVLink data Tx / Rx KiB counters of one GPU (nvidia-smi nvlink -gt d), or None."""
+    import re
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu)], capture_output=True, text=True,
+                             timeout=30).stdout
+    except Exception:
+        return None
+    tx = sum(int(x) for x in re.findall(r"Tx:\s*(\d+)\s*KiB", out))
+    rx = sum(int(x) for x in re.findall(r"Rx:\s*(\d+)\s*KiB", out))
+    return {"tx_kib": tx, "rx_kib": rx, "links": len(re.findall(r"Link \d+", out)) // 2 or None}
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -46,7 +60,14 @@ def main():
             for ctas in variants:
                 os.environ["RK_PEER_COPY_CTAS"] = str(ctas)
                 eng.peer_bandwidth(1, nbytes)      # warm
+                c0 = nvlink_counters(local)
                 res[f"{kind}_ctas{ctas}_gbs"] = max(eng.peer_bandwidth(1, nbytes) for _ in range(3))
+                c1 = nvlink_counters(local)
+                if c0 and c1:
+                    # rank 0 reads rank 1's home region: the bytes arrive on rank 0's links (Rx)
+                    res[f"{kind}_ctas{ctas}_nvlink"] = {"rx_gib": (c1["rx_kib"] - c0["rx_kib"]) / 2**20,
+                                                        "tx_gib": (c1["tx_kib"] - c0["tx_kib"]) / 2**20,
+                                                        "copied_gib": 3 * nbytes / 2**30, "links": c1["links"]}
             os.environ.pop("RK_PEER_COPY_CTAS", None)
         dist.barrier()
         eng.close()
