@@ -33,7 +33,7 @@ def nvlink_counters(gpu: int):
         return None
     tx = sum(int(x) for x in re.findall(r"Tx:\s*(\d+)\s*KiB", out))
     rx = sum(int(x) for x in re.findall(r"Rx:\s*(\d+)\s*KiB", out))
-    return {"tx_kib": tx, "rx_kib": rx, "links": len(re.findall(r"Link \d+", out)) // 2 or None}
+    return {"tx_kib": tx, "rx_kib": rx, "links": len(re.findall(r"Link \d+", out)) // 2 or None, "raw": out[:600]}
 
 
 def main():
@@ -63,6 +63,7 @@ def main():
                 c0 = nvlink_counters(local)
                 res[f"{kind}_ctas{ctas}_gbs"] = max(eng.peer_bandwidth(1, nbytes) for _ in range(3))
                 c1 = nvlink_counters(local)
+                res.setdefault("nvlink_raw_sample", (c1 or {}).get("raw"))
                 if c0 and c1:
                     # rank 0 reads rank 1's home region: the bytes arrive on rank 0's links (Rx)
                     res[f"{kind}_ctas{ctas}_nvlink"] = {"rx_gib": (c1["rx_kib"] - c0["rx_kib"]) / 2**20,
