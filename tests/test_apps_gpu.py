@@ -90,12 +90,15 @@ def test_cv_kernels_match_reference(name):
         assert [float(f).hex() for f in freqs] == [f.hex() for _, f in ref]   # count/total bit-exact
 
 
-def test_cv_engine_with_eviction_matches_reference():
+@pytest.mark.parametrize("host_slots", [0, 16])
+def test_cv_engine_with_eviction_matches_reference(host_slots):
+    """Tight device tier (7 slots for 16 items); with a 16-slot host tier every
+    document is preprocessed once (R = 1) and device misses are host hits."""
     _l, device = _mods()
     g = load("cv.json")["acceptance_c04b05_k3"]
     n = len(g["parsed"])
     eng = device.DeviceEngine(_l.app_params(_l.APP_CV, n, max_entries=256, threshold=0.5), leaf_block=3,
-                              device_slots=7)
+                              device_slots=7, host_slots=host_slots)
     app = device.DeviceApp(_l.app_params(_l.APP_CV, n, max_entries=256))
     host = pack_parsed(g["parsed"], app.parsed_bytes).pin_memory()
     out = torch.zeros(n * (n - 1) // 2, dtype=torch.float64, device="cuda")
@@ -103,7 +106,11 @@ def test_cv_engine_with_eviction_matches_reference():
     want = np.array([float.fromhex(v) for v in g["values"]])
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-15)
     st = eng.stats()
-    assert st["pairs_done"] == 120 and st["evictions"] > 0 and st["loads"] > n
+    assert st["pairs_done"] == 120 and st["evictions"] > 0 and st["ledger_marked"] == 120
+    if host_slots:
+        assert st["loads"] == n and st["host_hits"] > 0
+    else:
+        assert st["loads"] > n
 
 
 def test_cv_slot_overflow_and_malformed():
