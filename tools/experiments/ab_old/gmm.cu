@@ -61,8 +61,10 @@ __global__ void gmm_preprocess_kernel(const uint8_t* __restrict__ parsed, size_t
 // shared memory as (x, y, s^2 + s0, |q|^2) and is read by broadcast.  The
 // rotation leaves |p| unchanged, so per (a, b, k)
 //   -|R_k p - q|^2 w = (2 (R_k p).q - |p|^2 - |q|^2) w,   w = log2(e) / (s_a^2 + s_b^2)
-// costs one FMUL + two FFMA + one MUFU.EX2 (+ the add): the reciprocal is shared
-// by the 12 angles of a block, so the kernel is bound by the SFU's ex2 rate.
+// costs one FMUL + two FFMA + one MUFU.EX2 (+ the add), done for two angles at a
+// time as packed fp32 pairs (FMUL2 / FFMA2 / FADD2); the reciprocal is shared by
+// the 12 angles of a block, so the kernel is bound by the SFU's ex2 rate (moving
+// 2 or 3 of the 12 exponentials to an FMA-pipe polynomial measured slower).
 constexpr int kPairWarps = 8;
 constexpr int kAngBlock = 12;
 
@@ -71,29 +73,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-
-// 2^x for x <= 0 on the FMA pipe (no MUFU): round-to-nearest split x = j + f via
-// the 1.5 * 2^23 magic constant, degree-5 polynomial for 2^f on [-0.5, 0.5]
-// (relative error 7.7e-8), exponent added as an integer.  Arguments below -125
-// return ~0 (the Gauss terms there are < 1e-37 of the peak).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.0f);
-  const float t = x + 12582912.0f;
-  const int j = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.0f);
-  float p = fmaf(0.0013266970386325856f, f, 0.00967545974551767f);
-  p = fmaf(p, f, 0.0555074261600255f);
-  p = fmaf(p, f, 0.24022121753561645f);
-  p = fmaf(p, f, 0.6931469491610631f);
-  p = fmaf(p, f, 1.0000000710296983f);
-  return __int_as_float(__float_as_int(p) + (j << 23));
-}
-
-// angles of a block whose exponentials go to the FMA pipe instead of the SFU,
-// balancing the two pipes (the kernel is SFU-bound otherwise)
-#ifndef GMM_POLY
-#define GMM_POLY 0   // measured: 0 (all MUFU) 478 ms, 2: 489 ms, 3: 500 ms per C4 job
-#endif
 
 // grid = pairs x angle blocks: CTA (p, ab) evaluates angles 12ab .. 12ab+11 of
 // pair p and stores its best E_k in blk_best[p * nblk + ab]; gmm_finalize takes
@@ -131,21 +110,25 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob
   const int units = n_chunks * 4;
   const int qlen = (mj + 3) / 4;
   {
-    float acc[kAngBlock];
+    // per angle pair: the two angles' running sums (fp32 lanes of one FADD2)
+    float2 acc2[kAngBlock / 2];
 #pragma unroll
-    for (int t = 0; t < kAngBlock; ++t) acc[t] = 0.f;
+    for (int t = 0; t < kAngBlock / 2; ++t) acc2[t] = make_float2(0.f, 0.f);
     for (int u = warp; u < units; u += kPairWarps) {
       const int a = (u >> 2) * 32 + lane;
       const int c0 = (u & 3) * qlen, c1 = min(mj, c0 + qlen);
       if (a < mi) {
         const float px = pi[3 * a], py = pi[3 * a + 1], sa = pi[3 * a + 2];
         const float pp = fmaf(px, px, py * py);
-        float rx[kAngBlock], ry[kAngBlock];
+        // the rotated point for two angles at a time as packed fp32 pairs: the
+        // FMUL2 / FFMA2 / FADD2 forms give the scalar results bit for bit with half
+        // the issue slots, leaving the MUFU.EX2 pipe as the only limit
+        float2 rx[kAngBlock / 2], ry[kAngBlock / 2];
 #pragma unroll
-        for (int t = 0; t < kAngBlock; ++t) {
-          const float2 w = s_cs[t];
-          rx[t] = w.x * px - w.y * py;
-          ry[t] = w.y * px + w.x * py;
+        for (int t = 0; t < kAngBlock; t += 2) {
+          const float2 wa = s_cs[t], wb = s_cs[t + 1];
+          rx[t / 2] = make_float2(wa.x * px - wa.y * py, wb.x * px - wb.y * py);
+          ry[t / 2] = make_float2(wa.y * px + wa.x * py, wb.y * px + wb.x * py);
         }
         for (int c = c0; c < c1; ++c) {
           const float4 q = Q[c];
@@ -153,10 +136,10 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob
           const float w2 = 2.0f * w;
           const float base = -(pp + q.w) * w;
 #pragma unroll
-          for (int t = 0; t < kAngBlock; ++t) {
-            const float dot = fmaf(rx[t], q.x, ry[t] * q.y);
-            const float arg = fmaf(dot, w2, base);
-            acc[t] += (t < GMM_POLY) ? ex2_poly(arg) : ex2_approx(arg);
+          for (int t = 0; t < kAngBlock / 2; ++t) {
+            const float2 dot = __ffma2_rn(rx[t], make_float2(q.x, q.x), __fmul2_rn(ry[t], make_float2(q.y, q.y)));
+            const float2 arg = __ffma2_rn(dot, make_float2(w2, w2), make_float2(base, base));
+            acc2[t] = __fadd2_rn(acc2[t], make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
           }
         }
       }
@@ -164,7 +147,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob
     // warp sums, then a fixed-order sum over the warps
 #pragma unroll
     for (int t = 0; t < kAngBlock; ++t) {
-      float v = acc[t];
+      float v = (t & 1) ? acc2[t / 2].y : acc2[t / 2].x;
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) s_part[warp][t] = v;
