@@ -78,31 +78,6 @@ __device__ __forceinline__ float rcp_fma(float x) {
   return y;
 }
 
-// 2^x for two x <= 0 on the FMA pipe as packed fp32 pairs: round-to-nearest
-// split x = j + f (1.5 * 2^23 magic), degree-5 polynomial for 2^f on [-0.5, 0.5]
-// (relative error 7.7e-8), exponent added as an integer; arguments below -125
-// give ~0 (those Gauss terms are < 1e-37 of the peak).
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x = make_float2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
-  const float2 mg = make_float2(12582912.0f, 12582912.0f);
-  const float2 t = __fadd2_rn(x, mg);
-  const float2 f = __fadd2_rn(x, __fadd2_rn(mg, make_float2(-t.x, -t.y)));
-  float2 p = __ffma2_rn(make_float2(0.0013266970386325856f, 0.0013266970386325856f), f,
-                        make_float2(0.00967545974551767f, 0.00967545974551767f));
-  p = __ffma2_rn(p, f, make_float2(0.0555074261600255f, 0.0555074261600255f));
-  p = __ffma2_rn(p, f, make_float2(0.24022121753561645f, 0.24022121753561645f));
-  p = __ffma2_rn(p, f, make_float2(0.6931469491610631f, 0.6931469491610631f));
-  p = __ffma2_rn(p, f, make_float2(1.0000000710296983f, 1.0000000710296983f));
-  const int jx = __float_as_int(t.x) - 0x4B400000, jy = __float_as_int(t.y) - 0x4B400000;
-  return make_float2(__int_as_float(__float_as_int(p.x) + (jx << 23)),
-                     __int_as_float(__float_as_int(p.y) + (jy << 23)));
-}
-// angle pairs (of the block's 6) whose exponentials run on the FMA pipe instead of
-// the SFU, balancing the two pipes
-#ifndef GMM_POLY_PAIRS
-#define GMM_POLY_PAIRS 1
-#endif
-
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -174,9 +149,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) gmm_pair_kernel(const PairJob
           for (int t = 0; t < kAngBlock / 2; ++t) {
             const float2 dot = __ffma2_rn(rx[t], make_float2(q.x, q.x), __fmul2_rn(ry[t], make_float2(q.y, q.y)));
             const float2 arg = __ffma2_rn(dot, make_float2(w2, w2), make_float2(base, base));
-            const float2 e = (t >= kAngBlock / 2 - GMM_POLY_PAIRS) ? ex2_poly2(arg)
-                                                                   : make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
-            acc2[t] = __fadd2_rn(acc2[t], e);
+            acc2[t] = __fadd2_rn(acc2[t], make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
           }
         }
       }
