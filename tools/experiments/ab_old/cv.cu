@@ -180,69 +180,6 @@ __global__ void __launch_bounds__(1024) cv_units(const PairJob job, const uint8_
   }
 }
 
-// One merge-path unit: A tokens [i, i_end) against B from j, in coalesced
-// 32-token windows (each lane binary-searches its A token in the B window with
-// register shuffles; matches add fa * fb in fp64; the window whose last token is
-// smaller is consumed, the other advances by a ballot count; the next windows are
-// prefetched one step ahead).  K = uint32_t when every token of both items is
-// below 2^32 (same comparisons, same fma order as K = uint64_t), else uint64_t.
-// Returns the warp-summed dot product.
-template <typename K>
-__device__ __forceinline__ double merge_unit(const uint64_t* __restrict__ ta, const double* __restrict__ fa, int i,
-                                             int i_end, const uint64_t* __restrict__ tb, const double* __restrict__ fb,
-                                             int j, int nb, int lane) {
-  constexpr K kInf = (K)~0ull;   // sentinel: k-mer ids of UTF-8 text never reach the key maximum
-  auto lda = [&](int idx) { return idx < i_end ? (K)__ldg(ta + idx) : kInf; };
-  auto ldb = [&](int idx) { return idx < nb ? (K)__ldg(tb + idx) : kInf; };
-  // current windows (a, b) and the next ones (an, bn), loaded one iteration ahead
-  K a = lda(i + lane), an = lda(i + 32 + lane);
-  K b = ldb(j + lane), bn = ldb(j + 32 + lane);
-  double dot = 0.0;
-  while (i < i_end && j < nb) {
-    const int na_w = min(32, i_end - i);
-    const int nb_w = min(32, nb - j);
-    const K amax = __shfl_sync(0xffffffffu, a, na_w - 1);
-    const K bmax = __shfl_sync(0xffffffffu, b, nb_w - 1);
-    // lower_bound of a in the B window (lanes >= nb_w hold +inf)
-    int pos = 0;
-#pragma unroll
-    for (int step = 16; step; step >>= 1) {
-      const K probe = __shfl_sync(0xffffffffu, b, pos + step - 1);
-      if (probe < a) pos += step;
-    }
-    const K at = __shfl_sync(0xffffffffu, b, pos & 31);
-    if (a != kInf && pos < nb_w && at == a) dot = fma(__ldg(fa + i + lane), __ldg(fb + j + pos), dot);
-    int adv_a, adv_b;
-    if (amax < bmax) {          // A window done; B tokens <= amax done too
-      adv_a = na_w;
-      adv_b = __popc(__ballot_sync(0xffffffffu, b <= amax));
-    } else if (bmax < amax) {   // B window done; A tokens <= bmax were checked against it
-      adv_b = nb_w;
-      adv_a = __popc(__ballot_sync(0xffffffffu, a <= bmax));
-    } else {
-      adv_a = na_w;
-      adv_b = nb_w;
-    }
-    if (adv_a) {   // slide the A window from (a, an), prefetch the next one
-      const int src = lane + adv_a;
-      const K x0 = __shfl_sync(0xffffffffu, a, src & 31), x1 = __shfl_sync(0xffffffffu, an, src & 31);
-      a = src < 32 ? x0 : x1;
-      i += adv_a;
-      an = lda(i + 32 + lane);
-    }
-    if (adv_b) {
-      const int src = lane + adv_b;
-      const K x0 = __shfl_sync(0xffffffffu, b, src & 31), x1 = __shfl_sync(0xffffffffu, bn, src & 31);
-      b = src < 32 ? x0 : x1;
-      j += adv_b;
-      bn = ldb(j + 32 + lane);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  return dot;
-}
-
 __global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PairJob job, const uint8_t* __restrict__ slots,
                                                          size_t slot_stride, int cap, const int* __restrict__ offsets,
                                                          int* __restrict__ ctl, double* __restrict__ partial) {
@@ -274,11 +211,55 @@ __global__ void __launch_bounds__(kCvWarps * 32) cv_work(const PairJob job, cons
     int i = merge_path(ta, na, tb, nb, d0);
     int j = d0 - i;
     const int i_end = merge_path(ta, na, tb, nb, d1);
-    // both lists below 2^32 - 1 (the last, largest token of each; every k-mer id of
-    // k <= 4): the window search and slides shuffle 32-bit keys, one SHFL each
-    const bool k32 = na > 0 && nb > 0 && __ldg(ta + na - 1) < 0xFFFFFFFFull && __ldg(tb + nb - 1) < 0xFFFFFFFFull;
-    const double dot = k32 ? merge_unit<uint32_t>(ta, fa, i, i_end, tb, fb, j, nb, lane)
-                           : merge_unit<uint64_t>(ta, fa, i, i_end, tb, fb, j, nb, lane);
+  constexpr uint64_t kInf = ~0ull;   // sentinel: k-mer ids of UTF-8 text never reach 2^64 - 1
+    auto lda = [&](int idx) { return idx < i_end ? __ldg(ta + idx) : kInf; };
+    auto ldb = [&](int idx) { return idx < nb ? __ldg(tb + idx) : kInf; };
+    // current windows (a, b) and the next ones (an, bn), loaded one iteration ahead
+    uint64_t a = lda(i + lane), an = lda(i + 32 + lane);
+    uint64_t b = ldb(j + lane), bn = ldb(j + 32 + lane);
+    double dot = 0.0;
+    while (i < i_end && j < nb) {
+      const int na_w = min(32, i_end - i);
+      const int nb_w = min(32, nb - j);
+      const uint64_t amax = __shfl_sync(0xffffffffu, a, na_w - 1);
+      const uint64_t bmax = __shfl_sync(0xffffffffu, b, nb_w - 1);
+      // lower_bound of a in the B window (lanes >= nb_w hold +inf)
+      int pos = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint64_t probe = __shfl_sync(0xffffffffu, b, pos + step - 1);
+        if (probe < a) pos += step;
+      }
+      const uint64_t at = __shfl_sync(0xffffffffu, b, pos & 31);
+      if (a != kInf && pos < nb_w && at == a) dot = fma(__ldg(fa + i + lane), __ldg(fb + j + pos), dot);
+      int adv_a, adv_b;
+      if (amax < bmax) {          // A window done; B tokens <= amax done too
+        adv_a = na_w;
+        adv_b = __popc(__ballot_sync(0xffffffffu, b <= amax));
+      } else if (bmax < amax) {   // B window done; A tokens <= bmax were checked against it
+        adv_b = nb_w;
+        adv_a = __popc(__ballot_sync(0xffffffffu, a <= bmax));
+      } else {
+        adv_a = na_w;
+        adv_b = nb_w;
+      }
+      if (adv_a) {   // slide the A window from (a, an), prefetch the next one
+        const int src = lane + adv_a;
+        const uint64_t x0 = __shfl_sync(0xffffffffu, a, src & 31), x1 = __shfl_sync(0xffffffffu, an, src & 31);
+        a = src < 32 ? x0 : x1;
+        i += adv_a;
+        an = lda(i + 32 + lane);
+      }
+      if (adv_b) {
+        const int src = lane + adv_b;
+        const uint64_t x0 = __shfl_sync(0xffffffffu, b, src & 31), x1 = __shfl_sync(0xffffffffu, bn, src & 31);
+        b = src < 32 ? x0 : x1;
+        j += adv_b;
+        bn = ldb(j + 32 + lane);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) partial[u] = dot;
   }
 }
