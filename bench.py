@@ -438,7 +438,7 @@ def realengine_sample(args, n_items=16, lanes=1):
                     "real mode, one node, load stage included"}
 
 
-def reference_arm(args, world_env, rank):
+def reference_arm(args, rank):
     """`--impl reference`: the reference-side CPU path, timed like our arm (W + K steps)."""
     if rank != 0:
         return 0
@@ -1170,7 +1170,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return reference_arm(args, env_world, rank)
+        return reference_arm(args, rank)
     if env_world is None and args.gpus > 1:
         return relaunch(args.gpus)
     world = int(env_world or "1")

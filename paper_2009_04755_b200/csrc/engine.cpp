@@ -660,11 +660,11 @@ rk_status ncc_peer_run(rk_engine* e, double* d_out, uint8_t* d_flags, int64_t la
   std::vector<int> order;
   for (int b = 0; b < M; ++b)
     if (!with[b].empty() && subs[b].s == r) order.push_back(b);
-  for (int dd = 1; dd < M; ++dd)
-    for (int a0 : {mine.empty() ? 0 : mine[0]}) {
-      const int b = (a0 + dd) % M;
-      if (!with[b].empty() && subs[b].s != r) order.push_back(b);
-    }
+  const int a0 = mine.empty() ? 0 : mine[0];
+  for (int dd = 1; dd < M; ++dd) {
+    const int b = (a0 + dd) % M;
+    if (!with[b].empty() && subs[b].s != r) order.push_back(b);
+  }
   const size_t stride = e->slot_stride;
   while ((int)e->gstreams.size() < (int)mine.size()) {
     cudaStream_t st;
