@@ -443,23 +443,8 @@ void trace_end(rk_engine* e, int k, cudaStream_t st) {
   if (k >= 0) cudaEventRecord(e->tr[k].b, st);
 }
 
-// Launch order inside a batch (results land at pair_id, so any order is valid):
-// grouped by the left item.  The persistent compare grid runs its pairs in waves
-// (CTA c takes pairs c, c + grid, ...), so a wave then shares one or two left
-// items across ~grid/2 CTAs that stream the same spectrum columns at the same
-// time -- L2 hits instead of HBM reads.  RK_PAIR_ORDER=0 keeps the leaf order.
-static bool pair_order_by_left() {
-  static const bool on = [] {
-    const char* v = getenv("RK_PAIR_ORDER");
-    return !(v && *v == '0');
-  }();
-  return on;
-}
-
 rk_status flush_pairs(rk_engine* e, std::vector<rk_pair>& pend, double* d_out, uint8_t* d_flags) {
   if (pend.empty()) return RK_OK;
-  if (e->app->p.kind == RK_APP_PCE && pair_order_by_left())
-    std::stable_sort(pend.begin(), pend.end(), [](const rk_pair& x, const rk_pair& y) { return x.i < y.i; });
   if (e->loads_unsynced) {   // the batch reads slots loaded on the load stream
     RK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_loaded, 0));
     e->loads_unsynced = false;
