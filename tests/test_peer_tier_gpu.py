@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0, n=26):
+def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0, n=26, side=256, slots=10):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -27,8 +27,8 @@ def _rank(rank, world, port, ret, steal_chunk=0, delay0=0.0, n=26):
     try:
         from paper_2009_04755_b200.apps import PCEApp
         from paper_2009_04755_b200.engine import AllPairsEngine
-        app = PCEApp(n, side=256, cameras=3, seed=17, device=0)
-        eng = AllPairsEngine(app, leaf_block=4, device_slots=10, rank=rank, world=world, peer_tier=True,
+        app = PCEApp(n, side=side, cameras=3, seed=17, device=0)
+        eng = AllPairsEngine(app, leaf_block=4, device_slots=slots, rank=rank, world=world, peer_tier=True,
                              steal_chunk=steal_chunk)
         if rank == 0 and delay0 > 0:
             # rank 0 starts late (after the barrier): rank 1 runs dry and steals from it
@@ -170,3 +170,36 @@ def test_ncc_gram_over_the_peer_tier(world, n, side, slots):
     assert max(pairs) <= 2 * min(pairs)                           # circulant share: balanced
     led = outs[0][3]["ledger"]
     assert led["full"] == 1 and led["completed"] == total and led["dup_marks"] == 0
+
+
+def test_2048_peer_tier_two_ranks():
+    """The C3 item size through the C3 path (pce2k_pair, home items k % 2, the rest
+    fetched from the peer's home region, stealing on) with a device tier smaller
+    than n, against the float64 oracle."""
+    import torch.multiprocessing as mp
+    from oracle import pce as opce
+    from oracle import scheduler as osch
+    from paper_2009_04755_b200.apps import PCEApp
+    n, side, world = 12, 2048, 2
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, ret, 1, 0.0, n, side, 4)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([ret.get(timeout=600) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    total = n * (n - 1) // 2
+    values = outs[0][1] + outs[1][1]
+    flags = outs[0][2].astype(int) + outs[1][2].astype(int)
+    assert set(np.unique(flags)) <= {1, 3}
+    app = PCEApp(n, side=side, cameras=3, seed=17)
+    pats = np.stack([np.frombuffer(app.fetch_raw(app.path_for_key(k)), dtype=np.float32).reshape(side, side)
+                     for k in range(n)])
+    want = opce.pairs_batched(pats, [osch.pair_from_id(n, p) for p in range(total)], batch=4)
+    np.testing.assert_allclose(values, want, rtol=1e-4)
+    assert sum(o[3]["loads"] for o in outs) == n and all(o[3]["peer_fetches"] > 0 for o in outs)
+    led = outs[0][3]["ledger"]
+    assert led["full"] == 1 and led["completed"] == total
