@@ -705,7 +705,11 @@ def main_pce(args, rank, world, local_rank):
     params = params_fn(n)
     # N > 1: peer-GPU tier -- each rank preprocesses its home items (k % N == rank),
     # every other item it needs is copied from its home GPU over NVLink (CUDA IPC)
-    peer = world > 1
+    # NCC whose items fit every GPU: each rank keeps all items resident and takes its
+    # round-robin share of the Gram tiles (a C2-size Gram is only ~1.8 waves of
+    # 256 x 256 tiles on one GPU, too little to split into peer-fetched sub-blocks);
+    # the peer tier carries C3-Gram (home-only)
+    peer = world > 1 and (not ncc or streamed)
     steal = peer and not args.no_steal and not ncc     # the Gram deals its blocks statically
     if streamed:
         home_cnt = len(range(rank, n, world))
@@ -767,10 +771,19 @@ def main_pce(args, rank, world, local_rank):
                     device_items=None if (host_home is not None or streamed) else items,
                     parsed_stride=parsed_bytes)
             barrier()
-        elif host_all is not None:
-            eng.run(out, flags, host_items=host_all, parsed_stride=parsed_bytes)
         else:
-            eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+            if world > 1:   # the job's shared ledger on rank 0 (IPC), reset before the barrier
+                if not state["connected"]:
+                    eng.connect_peers()
+                    state["connected"] = True
+                eng.ledger_reset()
+                barrier()
+            if host_all is not None:
+                eng.run(out, flags, host_items=host_all, parsed_stride=parsed_bytes)
+            else:
+                eng.run(out, flags, device_items=items, parsed_stride=parsed_bytes)
+            if world > 1:
+                barrier()
 
     for _ in range(args.warmup):
         step()

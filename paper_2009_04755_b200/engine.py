@@ -113,9 +113,13 @@ class AllPairsEngine:
         self.world = world
         torch.cuda.set_device(app.device)
         slots = device_slots if device_slots is not None else app.n
+        # NCC: with every item resident (slots >= n) each rank takes its round-robin
+        # share of the Gram tiles; with fewer slots the Gram runs over home
+        # sub-blocks and peer-fetched partners (the peer tier)
+        ncc_resident = app.kind == 3 and slots >= app.n
         self._eng = DeviceEngine(app.app_params(), leaf_block=leaf_block, device_slots=max(2, slots),
                                  rank=rank, world=world, device=app.device,
-                                 peer_tier=peer_tier and world > 1 and app.kind != 0,
+                                 peer_tier=peer_tier and world > 1 and app.kind != 0 and not ncc_resident,
                                  steal=steal and world > 1 and app.kind != 3, steal_chunk=steal_chunk,
                                  host_slots=host_slots)
         self._peers_connected = False
