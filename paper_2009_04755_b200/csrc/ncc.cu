@@ -551,11 +551,8 @@ rk_status ncc_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
   RK_TRY(status_begin(app, s, &d_status));
   const size_t stride_f = parsed_stride / sizeof(float);
   constexpr int kParts = 64;
-  // chunks of items small enough (~40 MB) that the normalise pass re-reads them
-  // from L2 rather than HBM: one HBM read + one write per item instead of two reads
-  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (40ll << 20) / (d * 4)));
-  for (int base = 0; base < n_items; base += chunk) {
-    const int m = std::min(chunk, n_items - base);
+  for (int base = 0; base < n_items; base += kMaxBatch) {
+    const int m = std::min(kMaxBatch, n_items - base);
     const float* px = static_cast<const float*>(d_parsed) + (size_t)base * stride_f;
     ncc_moments<<<dim3(kParts, m), 256, 0, s>>>(px, stride_f, d, app->ncc.part);
     SlotList dst;
