@@ -152,21 +152,6 @@ __device__ __forceinline__ void radix2_last(float2 (&e)[32], float2 (&o)[32], fl
   }
 }
 
-// radix2_last with the step's twiddles W^(lane + R*k1) (forward sign) read from a
-// [k1][lane] shared table -- one conflict-free 8-byte load instead of forming
-// W^lane * W_64^k1 with a second complex multiply.
-template <bool INV>
-__device__ __forceinline__ void radix2_last_tab(float2 (&e)[32], float2 (&o)[32], const float2* tab, int lane) {
-#pragma unroll
-  for (int k1 = 0; k1 < 32; ++k1) {
-    float2 w = tab[k1 * 32 + lane];
-    if (INV) w.y = -w.y;
-    const float2 t = c_mul(o[k1], w);
-    o[k1] = c_sub(e[k1], t);
-    e[k1] = c_add(e[k1], t);
-  }
-}
-
 __host__ __device__ constexpr int bitrev_const(int i, int logn) {
   int r = 0;
   for (int b = 0; b < logn; ++b) r |= ((i >> b) & 1) << (logn - 1 - b);

@@ -240,12 +240,12 @@ __device__ __forceinline__ void argmax2k_update(const float2 (&e)[R], const floa
 // odd half at blk + kUnitF2): e <- columns lane + R*k1, o <- columns H + lane + R*k1.
 __device__ __forceinline__ void block_rows_c2r(float2 (&e)[R], float2 (&o)[R], const float2* even_half,
                                                const float2* odd_half, int rp, float2* xbuf, const float2* tw,
-                                               const float2* tw2, int lane) {
+                                               float2 wl, int lane) {
   block8_rows_z<R>(e, even_half, rp, lane);
   group_fft_pad<R, true>(e, xbuf, tw, lane);
   half_rows_zodd(o, odd_half, rp, lane);
   group_fft_pad<R, true>(o, xbuf, tw, lane);
-  radix2_last_tab<true>(e, o, tw2, lane);
+  radix2_last<true>(e, o, wl);
 }
 
 // Window energy of row pair (ra, ra + 1) from its staged 8-row block: the sum of
@@ -253,9 +253,9 @@ __device__ __forceinline__ void block_rows_c2r(float2 (&e)[R], float2 (&o)[R], c
 // Kept out of line so the cold window path does not raise the register
 // allocation (and spills) of the hot column and row passes.
 __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart, int pcol, float2* xbuf,
-                                          const float2* tw, const float2* tw2, int lane) {
+                                          const float2* tw, float2 wl, int lane) {
   float2 e[R], o[R];
-  block_rows_c2r(e, o, blk, blk + kUnitF2, (ra & 7) >> 1, xbuf, tw, tw2, lane);
+  block_rows_c2r(e, o, blk, blk + kUnitF2, (ra & 7) >> 1, xbuf, tw, wl, lane);
   const bool va = ((ra - rstart + N) & (N - 1)) < kWin;
   const bool vb = ((ra + 1 - rstart + N) & (N - 1)) < kWin;
   float w = 0.f;
@@ -293,7 +293,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
   float2* gbufs = smem;                                  // 2 groups x 2 units
   float2* tw = smem + 4 * kUnitF2;                       // R*R twiddles (W_1024)
   float2* xbufs = tw + R * R;                            // one padded transpose buffer per warp
-  float2* tw2 = xbufs + kWarps * kXbuf;                  // [k1][lane] W_2048^(lane + 32 k1) of the radix-2 step
   __shared__ __align__(8) uint64_t s_bar[2][3];          // per group: column units, row halves even / odd
   __shared__ __align__(8) uint64_t s_wbar;
   __shared__ __align__(8) uint64_t s_cbar[kWarps];        // per warp: its column (PCE2K_WARP_COLS)
@@ -314,11 +313,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
   float2* gb = gbufs + wg * 2 * kUnitF2;
   float2* Tp = T + (size_t)blockIdx.x * t_stride;
   for (int i = tid; i < R * R; i += kWarps * 32) tw[i] = tw_g[i];
-  for (int i = tid; i < 32 * 32; i += kWarps * 32) {
-    double sn, cs;
-    sincospi(-(double)((i & 31) + 32 * (i >> 5)) / 1024.0, &sn, &cs);   // W_2048^(lane + 32 k1), forward
-    tw2[i] = make_float2((float)cs, (float)sn);
-  }
   if (tid == 0) {
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
@@ -339,6 +333,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
 #else
 #define PCE2K_FFT(v) group_fft_pad<R, true>(v, xbuf, tw, lane)
 #endif
+  const float2 wl = lane_w2048(lane);
   const uint64_t pol = l2_policy_evict_normal();
   const uint64_t pol_first = l2_policy_evict_first();
 
@@ -429,7 +424,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         PCE2K_FFT(e);
         product(u + 1, o);
         PCE2K_FFT(o);
-        radix2_last_tab<true>(e, o, tw2, lane);
+        radix2_last<true>(e, o, wl);
         // row n = lane + R*k1 -> block (lane >> 3) + 4*k1, row lane & 7; row n + H -> block + 128
         const int j = col >> 1;
         const int rr = lane & 7;
@@ -482,7 +477,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
           issue(rb + 2, 1);
         }
         PCE2K_FFT(o);
-        radix2_last_tab<true>(e, o, tw2, lane);
+        radix2_last<true>(e, o, wl);
         argmax2k_update(e, o, 8 * rb + 2 * gi, lane, m, idx, ss);
       }
     }
@@ -533,7 +528,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         mbar_wait(&s_wbar, wph & 1u);
         wph ^= 1u;
         if (warp < kPairsOfRows && (ra >> 3) == blk) {
-          const float w = window_rows(gbufs, ra, rstart, pcol, xbuf, tw, tw2, lane);
+          const float w = window_rows(gbufs, ra, rstart, pcol, xbuf, tw, wl, lane);
           if (lane == 0) s_wpart[warp] = w;
         }
         __syncthreads();   // staged block consumed before the next one lands
@@ -555,7 +550,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
 
 constexpr size_t kRowsFwdSmem = (size_t)(NC * kP1Tile + 4 * N) * sizeof(float2);
 constexpr size_t kColsFwdSmem = (size_t)(kWarps * kXbuf) * sizeof(float2);
-constexpr size_t kPairSmem = (size_t)(4 * kUnitF2 + R * R + kWarps * kXbuf + 32 * 32) * sizeof(float2);
+constexpr size_t kPairSmem = (size_t)(4 * kUnitF2 + R * R + kWarps * kXbuf) * sizeof(float2);
 
 }  // namespace
 
