@@ -1,6 +1,12 @@
 """C3-Gram NCC: zero-lag NCC of N = 16,384 items of 2048^2 fp32
 (256 GiB; no GPU holds them all) as a blocked tcgen05 Gram over the GPUs of one box.
 
+Round-1 standalone version over the C ABI (contiguous key blocks, serpentine
+owners).  Since round 2 the engine itself runs this job over the peer tier
+(`ncc_peer_run`; `bench.py --gpus N --app ncc --items 16384 --side 2048`,
+`AllPairsEngine` with device_slots < n); this script is kept as the comparison
+point quoted in DESIGN.md.
+
   python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \\
       --master-port 29700 tools/c3_ncc.py [--items 16384] [--side 2048] [--block 2048]
 
