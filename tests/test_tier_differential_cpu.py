@@ -89,3 +89,49 @@ def test_tier_matches_reference_cache_tier(capacity, seq):
         assert [lib.rk_tier_slot_key(t, s) for s in range(capacity)] == want
     finally:
         lib.rk_tier_destroy(t)
+
+
+@settings(max_examples=60, deadline=None)
+@given(n=st.integers(0, 700), leaf=st.integers(1, 40))
+def test_quadtree_leaves_match_reference(n, leaf):
+    """librocket's depth-first leaves (rk_leaves, world 1) are the reference's
+    iter_leaves(root_region(n), leaf) in order, for random n and leaf sizes."""
+    _ref_modules()
+    from allpairs.scheduler import iter_leaves, root_region
+    from paper_2009_04755_b200.engine import rank_leaves
+    want = [r.as_tuple() for r in iter_leaves(root_region(n), leaf)] if n > 1 else []
+    assert rank_leaves(n, leaf) == want
+
+
+@settings(max_examples=200, deadline=None)
+@given(n=st.integers(2, 5000), data=st.data())
+def test_pair_id_matches_reference_ledger(n, data):
+    """rk_pair_id (the result-matrix index every kernel writes) is PairLedger.pair_id."""
+    _ref_modules()
+    from allpairs.scheduler import PairLedger
+    from paper_2009_04755_b200._lib import lib
+    i = data.draw(st.integers(0, n - 2))
+    j = data.draw(st.integers(i + 1, n - 1))
+    assert lib.rk_pair_id(n, i, j) == PairLedger(n).pair_id(i, j)
+
+
+@settings(max_examples=100, deadline=None)
+@given(n=st.integers(1, 100000), r=st.floats(1.0, 50.0), p=st.integers(1, 64),
+       costs=st.tuples(*[st.floats(0.0, 1e-2)] * 4), mfb=st.floats(0.0, 1e8), bw=st.floats(1e6, 1e11),
+       t=st.floats(1e-3, 1e5))
+def test_perf_model_matches_reference(n, r, p, costs, mfb, bw, t):
+    """The perf model the bench reports (T_min, efficiency, per-resource bounds)
+    equals the reference's perfmodel.py on random inputs."""
+    _ref_modules()
+    from allpairs import perfmodel as ref
+    from paper_2009_04755_b200 import perfmodel as ours
+    kw = dict(t_parse=costs[0], t_preprocess=costs[1], t_comparison=costs[2], t_postprocess=costs[3],
+              mean_file_bytes=mfb, io_bandwidth=bw)
+    rc, oc = ref.StageCosts(**kw), ours.StageCosts(**kw)
+    assert ours.t_min(n, oc) == ref.t_min(n, rc)
+    assert ours.t_gpu(n, r, oc) == ref.t_gpu(n, r, rc)
+    assert ours.t_cpu(n, r, oc) == ref.t_cpu(n, r, rc)
+    assert ours.t_io(n, r, oc) == ref.t_io(n, r, rc)
+    tm = ours.t_min(n, oc)
+    if tm > 0:
+        assert ours.efficiency(tm, p, t) == ref.efficiency(tm, p, t)
