@@ -72,6 +72,7 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-steal", action="store_true", help="N > 1: static leaf shares, no cross-GPU stealing")
+    ap.add_argument("--steal-chunk", type=int, default=0, help="N > 1: leaves per work-queue grab (0: one batch)")
     ap.add_argument("--trace-dir", default="",
                     help="pce: after the timed steps, run one traced step and write the reference-schema "
                          "trace (JSONL) and run-metrics document of each rank here")
@@ -725,7 +726,7 @@ def main_pce(args, rank, world, local_rank):
     else:
         dslots = n
     eng = device.DeviceEngine(params, leaf_block=args.leaf, device_slots=dslots, rank=rank, world=world,
-                              device=local_rank, peer_tier=peer, steal=steal)
+                              device=local_rank, peer_tier=peer, steal=steal, steal_chunk=args.steal_chunk)
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
@@ -1042,7 +1043,7 @@ def main_app(args, rank, world, local_rank):
         work = 16.0 * (n - 1) * float(nnz.sum())   # sum over pairs of 16 (nnz_i + nnz_j) bytes
     multi = world > 1
     eng = device.DeviceEngine(params, leaf_block=16, device_slots=n, rank=rank, world=world, device=local_rank,
-                              peer_tier=multi, steal=multi and not args.no_steal)
+                              peer_tier=multi, steal=multi and not args.no_steal, steal_chunk=args.steal_chunk)
     out = torch.zeros(pairs_total, dtype=torch.float64, device="cuda")
     flags = torch.zeros(pairs_total, dtype=torch.uint8, device="cuda")
     estream = torch.cuda.ExternalStream(eng.stream())
