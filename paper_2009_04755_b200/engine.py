@@ -144,9 +144,19 @@ class AllPairsEngine:
         return host
 
     def run(self, host_items: Optional[torch.Tensor] = None, device_items: Optional[torch.Tensor] = None,
-            gather: bool = True) -> RunResult:
-        """One full all-pairs job; returns the packed triangle (on rank 0 when world > 1)."""
-        if host_items is None and device_items is None and self.app.kind != 0:
+            gather: bool = True, home_chunks=None, chunk: int = 256) -> RunResult:
+        """One full all-pairs job; returns the packed triangle (on rank 0 when world > 1).
+
+        Items come from ``host_items`` / ``device_items`` (all n at the parsed
+        stride), from the app's own fetch_raw + parse, or -- with the peer tier, for
+        jobs whose items exist on no single GPU or host (C3) -- from
+        ``home_chunks(m0, count)``, which returns this rank's home items m0 ..
+        m0 + count - 1 (keys rank + m * world) as one host or device tensor at the
+        parsed stride; they are preprocessed ``chunk`` at a time into the home region.
+        """
+        if home_chunks is not None and not self._eng.peer_tier:
+            raise ValueError("home_chunks needs the peer tier (world > 1)")
+        if host_items is None and device_items is None and home_chunks is None and self.app.kind != 0:
             host_items = self.load_items()
         self._out.zero_()
         self._flags.zero_()
@@ -156,7 +166,14 @@ class AllPairsEngine:
         # world > 1: the ranks share rank 0's exactly-once ledger over IPC (and, with the
         # peer tier / stealing, each other's home regions and queue words)
         shared = self.world > 1
-        if self._eng.peer_tier:
+        if home_chunks is not None:
+            n_home = len(range(self.rank, self.app.n, self.world))
+            for m0 in range(0, n_home, chunk):
+                cnt = min(chunk, n_home - m0)
+                part = home_chunks(m0, cnt)
+                kw = {"device_items": part} if part.is_cuda else {"host_items": part}
+                self._eng.load_home_range(m0, cnt, parsed_stride=stride, **kw)
+        elif self._eng.peer_tier:
             # home items first (k % world == rank), then the IPC-mapped peer homes
             # home item m = key rank + m*world: a strided view of the full item array
             off = self.rank * stride

@@ -203,3 +203,56 @@ def test_2048_peer_tier_two_ranks():
     assert sum(o[3]["loads"] for o in outs) == n and all(o[3]["peer_fetches"] > 0 for o in outs)
     led = outs[0][3]["ledger"]
     assert led["full"] == 1 and led["completed"] == total
+
+
+def _chunk_rank(rank, world, port, ret, n, side):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2009_04755_b200 import device
+        from paper_2009_04755_b200.apps import PCEApp
+        from paper_2009_04755_b200.engine import AllPairsEngine
+        app = PCEApp(n, side=side, cameras=3, seed=23, device=0)
+        eng = AllPairsEngine(app, leaf_block=4, device_slots=6, rank=rank, world=world)
+        buf = torch.empty(4 * side * side, dtype=torch.float32, device="cuda")
+
+        def home_chunks(m0, count):   # this rank's home items, generated where they live (C3 style)
+            for q in range(count):
+                device.synth_prnu(side, side, rank + (m0 + q) * world, 1, 3, 23,
+                                  buf[q * side * side:(q + 1) * side * side])
+            return buf
+        res = eng.run(gather=False, home_chunks=home_chunks, chunk=4)
+        ret.put((rank, res.values.copy(), res.flags.copy(), dict(res.stats, ledger=res.ledger)))
+        eng.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_public_api_home_chunks():
+    """AllPairsEngine.run(home_chunks=...): no rank ever holds all items -- each
+    generates its home items chunk by chunk where they live, the rest arrive over
+    the peer tier (the C3 placement through the public API)."""
+    import torch.multiprocessing as mp
+    from oracle import pce as opce
+    from paper_2009_04755_b200.apps import PCEApp
+    n, side, world = 22, 256, 2
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_rank, args=(r, world, port, ret, n, side)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([ret.get(timeout=300) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    values = outs[0][1] + outs[1][1]
+    app = PCEApp(n, side=side, cameras=3, seed=23)
+    pats = np.stack([np.frombuffer(app.fetch_raw(app.path_for_key(k)), dtype=np.float32).reshape(side, side)
+                     for k in range(n)])
+    np.testing.assert_allclose(values, opce.all_pairs(pats), rtol=1e-4)
+    assert sum(o[3]["loads"] for o in outs) == n
+    assert outs[0][3]["ledger"]["full"] == 1
