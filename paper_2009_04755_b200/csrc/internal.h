@@ -137,6 +137,8 @@ struct PceState {
   float2* T = nullptr;     // clusters * t_stride: column-pass output, one slot per cluster
   size_t t_stride = 0;     // float2 between T slots: (N/2)*N + padding (breaks the power-of-two stride)
   PairJob* job = nullptr;   // host staging of the launch parameters
+  unsigned* rounds = nullptr;   // round-barrier counter of the compare grid (RK_PCE_LOCKSTEP), else null
+  int l2opts = 0;           // RK_PCE_L2OPTS: bit 0 T stores evict_first, bit 1 spectra evict_last
 };
 
 struct CvState {};
@@ -177,6 +179,9 @@ rk_status pce_preprocess(rk_app* app, const void* d_parsed, size_t parsed_stride
 
 // 2048^2 variant (pce2k.cu) and the shared mean-reduction launch (pce.cu)
 rk_status pce2k_init(rk_app* app);
+// Compare-grid round barrier + L2 options of the PCE kernels (env RK_PCE_LOCKSTEP,
+// RK_PCE_L2OPTS), set up at app creation (pce.cu).
+rk_status pce_round_init(PceState& st, int l2opts_default);
 rk_status pce2k_preprocess(rk_app* app, const float* pix, size_t stride_f, int n_items, char* slots,
                            size_t slot_stride, const int32_t* h_slot_idx, cudaStream_t s);
 rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, const rk_pair* pairs, int n,

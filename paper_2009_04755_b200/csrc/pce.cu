@@ -35,6 +35,7 @@
 
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -205,7 +206,7 @@ template <int R, int CL>
 __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     const PairJob job, const char* __restrict__ slots, size_t slot_stride, float2* __restrict__ T, size_t t_stride,
     const float2* __restrict__ tw_g, double* __restrict__ out, uint8_t* __restrict__ flags, double threshold,
-    const LedgerRef ledger) {
+    const LedgerRef ledger, unsigned* __restrict__ rounds, int l2opts) {
   constexpr int N = R * R;
   constexpr int G = 32 / R;               // lane groups per warp
   constexpr int kCtaWarps = cta_warps(R);
@@ -269,11 +270,12 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   // special priority (evict_last / evict_first measured within 1 %); T blocks are
   // read once, evict_first.
   const uint64_t pol_first = l2_policy_evict_first();
-  const uint64_t pol_T = l2_policy_evict_normal();
-  const uint64_t pol_spec = pol_T;
+  const uint64_t pol_T = (l2opts & 1) ? pol_first : l2_policy_evict_normal();
+  const uint64_t pol_spec = (l2opts & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();
   cluster_sync();
 
   for (int pi = cid; pi < job.npairs; pi += ncl) {
+    if (CL == 1) round_wait(rounds, pi, ncl, tid);
     const DevPair pr = job.pairs[pi];
     float2 v[R];
     PCE_PROBE(0);
@@ -485,6 +487,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       ledger_mark(ledger, pr.pid);
       if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
     }
+    if (CL == 1) round_arrive(rounds, tid);
   }
 }
 
@@ -563,10 +566,12 @@ rk_status compare_impl(rk_app* app, const char* slots, size_t slot_stride, const
     job.pairs[k].pid = pair_id(app->p.n, pairs[k].i, pairs[k].j);
   }
   const int clusters = std::min(st.clusters, n);
+  unsigned* rounds = CL == 1 ? st.rounds : nullptr;
+  if (rounds) RK_CUDA(cudaMemsetAsync(rounds, 0, sizeof(unsigned), s));
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = cluster_config<R>(clusters * CL, s, attr);
   RK_CUDA(cudaLaunchKernelEx(&cfg, pce_cluster<R, CL>, job, slots, slot_stride, st.T, st.t_stride, (const float2*)st.tw, d_out,
-                             d_flags, threshold_or_nan(app), app->ledger));
+                             d_flags, threshold_or_nan(app), app->ledger, rounds, st.l2opts));
   app->launches += 1;
   return RK_OK;
 }
@@ -585,7 +590,7 @@ rk_status cluster_init(rk_app* app) {
   st.t_stride = (size_t)(N / 2) * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * clusters));
   st.job = new PairJob();
-  return RK_OK;
+  return pce_round_init(st, 0);
 }
 
 }  // namespace
@@ -651,8 +656,20 @@ rk_status pce_init(rk_app* app) {
   return cluster_init<32>(app);
 }
 
+// Defaults measured on B200 (profiles/r2_ab_lockstep.json): the round
+// barrier on at every size; at 2048^2 T stores evict_first + spectra evict_last
+// (84.4k -> 104.9k pairs/s with the barrier), at 1024^2 no L2 hints (neutral).
+rk_status pce_round_init(PceState& st, int l2opts_default) {
+  const char* e = getenv("RK_PCE_LOCKSTEP");
+  if (e == nullptr || atoi(e) != 0) RK_CUDA(cudaMalloc(&st.rounds, sizeof(unsigned)));
+  const char* o = getenv("RK_PCE_L2OPTS");
+  st.l2opts = o ? atoi(o) : l2opts_default;
+  return RK_OK;
+}
+
 void pce_free(rk_app* app) {
   PceState& st = app->pce;
+  cudaFree(st.rounds);
   cudaFree(st.tw);
   cudaFree(st.T);
   cudaFree(st.U);

@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
                                                             size_t slot_stride, float2* __restrict__ T, size_t t_stride,
                                                             const float2* __restrict__ tw_g, double* __restrict__ out,
                                                             uint8_t* __restrict__ flags, double threshold,
-                                                            const LedgerRef ledger) {
+                                                            const LedgerRef ledger, unsigned* __restrict__ rounds,
+                                                            int l2opts) {
   constexpr int kGW = kWarps / 2;                        // warps per warp group
   constexpr int kPairsOfRows = (kWin + 1) / 2;
   extern __shared__ __align__(128) float2 smem[];
@@ -334,10 +335,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
 #define PCE2K_FFT(v) group_fft_pad<R, true>(v, xbuf, tw, lane)
 #endif
   const float2 wl = lane_w2048(lane);
-  const uint64_t pol = l2_policy_evict_normal();
   const uint64_t pol_first = l2_policy_evict_first();
+  const uint64_t pol = (l2opts & 2) ? l2_policy_evict_last() : l2_policy_evict_normal();   // spectra
+  const uint64_t pol_T = (l2opts & 1) ? pol_first : l2_policy_evict_normal();
 
   for (int pi = blockIdx.x; pi < job.npairs; pi += gridDim.x) {
+    round_wait(rounds, pi, gridDim.x, tid);
     const DevPair pr = job.pairs[pi];
     const float2* Xs = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_a * slot_stride);
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);
@@ -434,8 +437,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         constexpr size_t kHalfRows = (size_t)(H / 8) * 2 * (NC / 2) * 8;
 #pragma unroll
         for (int k1 = 0; k1 < R; ++k1) {
-          stg_hint(dst + k1 * kStep, e[k1], pol);
-          stg_hint(dst + kHalfRows + k1 * kStep, o[k1], pol);
+          stg_hint(dst + k1 * kStep, e[k1], pol_T);
+          stg_hint(dst + kHalfRows + k1 * kStep, o[k1], pol_T);
         }
       }
     }
@@ -544,6 +547,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
       ledger_mark(ledger, pr.pid);
       if (flags) flags[pr.pid] = isnan(threshold) ? 0 : (uint8_t)(1 | (pce >= threshold ? 2 : 0));
     }
+    round_arrive(rounds, tid);
     __syncthreads();   // shared state and buffers free for the next pair
   }
 }
@@ -568,7 +572,7 @@ rk_status pce2k_init(rk_app* app) {
   st.t_stride = (size_t)NC * N + stride_pad("RK_T_PAD", 0) / sizeof(float2);
   RK_CUDA(cudaMalloc(&st.T, sizeof(float2) * st.t_stride * st.clusters));
   st.job = new PairJob();
-  return RK_OK;
+  return pce_round_init(st, 3);
 }
 
 rk_status pce2k_preprocess(rk_app* app, const float* pix, size_t stride_f, int n_items, char* slots,
@@ -601,8 +605,9 @@ rk_status pce2k_compare(rk_app* app, const char* slots, size_t slot_stride, cons
     job.pairs[k].pid = pair_id(app->p.n, pairs[k].i, pairs[k].j);
   }
   const int grid = std::min(st.clusters, n);
+  if (st.rounds) RK_CUDA(cudaMemsetAsync(st.rounds, 0, sizeof(unsigned), s));
   pce2k_pair<<<grid, kWarps * 32, kPairSmem, s>>>(job, slots, slot_stride, st.T, st.t_stride, st.tw, d_out, d_flags,
-                                                   threshold_or_nan(app), app->ledger);
+                                                   threshold_or_nan(app), app->ledger, st.rounds, st.l2opts);
   app->launches += 1;
   RK_CUDA(cudaGetLastError());
   return RK_OK;

@@ -81,6 +81,28 @@ __device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Round barrier of the persistent compare grids.  Round k of a launch is pairs
+// [k*G, (k+1)*G) (one per CTA); with `rounds` set, a CTA starts its round-k pair
+// only when all G CTAs have finished round k-1, so the in-flight pairs (which the
+// engine's leaf order draws from a few items) read the same spectrum columns at
+// the same time and share them through L2 instead of drifting apart.  It is a
+// timing barrier only: a CTA stops waiting after kRoundSpin cycles, so partial
+// residency (another kernel holding SMs) can slow it but never deadlock it.
+constexpr long long kRoundSpin = 200000;
+__device__ __forceinline__ void round_wait(const unsigned* rounds, int pi, int G, int tid) {
+  if (rounds == nullptr || pi < G) return;
+  if (tid == 0) {
+    const unsigned target = (unsigned)(pi / G) * (unsigned)G;   // arrivals of rounds 0 .. k-1
+    const long long t0 = clock64();
+    while (ld_acquire(rounds) < target && clock64() - t0 < kRoundSpin) __nanosleep(64);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void round_arrive(unsigned* rounds, int tid) {
+  if (rounds != nullptr && tid == 0) red_release_add(rounds, 1u);
+}
+
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
