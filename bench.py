@@ -620,7 +620,13 @@ def calibrate_pce(args, params_fn, side, cameras, seed):
     import ctypes as C
 
     from paper_2009_04755_b200 import _lib
-    plist = [(i, j, i, j) for i in range(m) for j in range(i + 1, m)]
+    # pairs in the engine's leaf order (leaf_block x leaf_block blocks of the
+    # triangle, pairs row-major inside a block): a round of the persistent compare
+    # grid then draws on as few spectra as it does in a job
+    lb = max(1, args.leaf)
+    plist = [(i, j, i, j) for bi in range(0, m, lb) for bj in range(bi, m, lb)
+             for i in range(bi, min(bi + lb, m)) for j in range(max(bj, i + 1), min(bj + lb, m))]
+    assert len(plist) == m * (m - 1) // 2
     pairs = (_lib.Pair * len(plist))(*[_lib.Pair(*p) for p in plist])   # built once: no host gaps
     out = torch.zeros(m * (m - 1) // 2, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()
