@@ -371,6 +371,40 @@ def test_compare_is_deterministic_run_to_run(side, n, runs):
         np.testing.assert_array_equal(o, outs[0])
 
 
+@pytest.mark.parametrize("side,n", [(1024, 40), (2048, 24)])
+def test_round_barrier_and_l2_hints_do_not_change_results(side, n, monkeypatch):
+    """The compare grid's round barrier (RK_PCE_LOCKSTEP) and L2 hints
+    (RK_PCE_L2OPTS) only change timing: with them on (the defaults) and off, the
+    same job gives bit-identical PCE values, including a launch whose last round
+    is partial (n = 40: 780 pairs = 5 rounds of 148 + 40); the defaults match the
+    float64 oracle on a sample."""
+    _l, device = _lib()
+    items = make_items(n, side, cameras=6, seed=23)
+    total = n * (n - 1) // 2
+    outs = {}
+    for lock, l2 in (("1", None), ("0", "0"), ("1", "3")):
+        monkeypatch.setenv("RK_PCE_LOCKSTEP", lock)
+        if l2 is None:
+            monkeypatch.delenv("RK_PCE_L2OPTS", raising=False)
+        else:
+            monkeypatch.setenv("RK_PCE_L2OPTS", l2)
+        eng = device.DeviceEngine(_l.app_params(_l.APP_PCE, n, height=side, width=side), leaf_block=8,
+                                  device_slots=n)
+        out = torch.full((total,), float("nan"), dtype=torch.float64, device="cuda")
+        eng.run(out, device_items=items, parsed_stride=side * side * 4)
+        outs[(lock, l2)] = out.cpu().numpy()
+        eng.close()
+    base = outs[("1", None)]
+    assert np.isfinite(base).all()
+    for o in outs.values():
+        np.testing.assert_array_equal(o, base)
+    host = items.cpu().numpy().reshape(n, side, side)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    pick = np.random.default_rng(5).choice(total, size=8, replace=False)
+    want = opce.pairs_batched(host, [pairs[p] for p in pick])
+    np.testing.assert_allclose(base[pick], want, rtol=RTOL)
+
+
 def test_synthetic_patterns_match_the_oracle_generator():
     """rk_synth_prnu (the bench's storage stage) against its float64 restatement
     (oracle/pce.py prnu_patterns) to fp32 rounding, and bit-identical whether items
