@@ -56,6 +56,10 @@ constexpr int kTileStride = kRows + 1;  // padded row stride of the [k][row] til
 // (8 warps at R = 32, 4 warps of two half-warp lane groups at R = 16).
 __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
 __host__ __device__ constexpr int xpose_size(int R) { return R * R; }   // XOR-swizzled transpose buffer
+// Row-phase buffer release by counted arrival (1) or a group barrier (0).
+#ifndef PCE_ROW_ARRIVE
+#define PCE_ROW_ARRIVE 0
+#endif
 template <int R>
 __device__ __forceinline__ void compare_fft(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {
   group_fft_rt<R, true>(v, xbuf, w, lane);
@@ -226,6 +230,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   float2* tw = smem + 2 * kNG * kHalf;    // R*R twiddles
   float2* xbufs = tw + R * R;             // one R*R transpose buffer per lane group
   __shared__ __align__(8) uint64_t s_bar[kNG][3];   // per group: column slices, row block 0 / 1
+  __shared__ unsigned s_done[kNG][2];   // per group and row buffer: warps done reading (PCE_ROW_ARRIVE)
   __shared__ __align__(8) uint64_t s_wbar;
   __shared__ __align__(8) uint64_t s_cbar[kCtaWarps];   // per warp: its column slice
   __shared__ float4 s_part[CL];           // CTA partials, gathered in CTA 0
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
     mbar_init(&s_wbar, 1);
     for (int w = 0; w < kCtaWarps; ++w) mbar_init(&s_cbar[w], 1);
+    for (int w = 0; w < kNG; ++w) s_done[w][0] = s_done[w][1] = 0u;
   }
   uint32_t ph = 0;                        // parity bits of this group's three barriers (bit b)
   uint32_t wph = 0;
@@ -375,6 +381,19 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
         mbar_wait(&s_bar[wg][1 + buf], (ph >> (1 + buf)) & 1u);
         ph ^= 2u << buf;
         block8_rows_z<R>(v, gb + buf * kHalf, gi, lane);
+#if PCE_ROW_ARRIVE
+        // the block is consumed once all kGW warps have read their row pair: the
+        // last warp to finish reading (acq_rel count) refills it, the others go
+        // straight on to their FFT instead of waiting at a group barrier
+        __syncwarp();
+        if (wl == 0 && rb + 2 * kNG < bend &&
+            atom_acq_rel_add_shared(&s_done[wg][buf], 1u) % kGW == (unsigned)(kGW - 1)) {
+          refill_fence();
+          mbar_expect_tx(&s_bar[wg][1 + buf], kHalfBytes);
+          bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 2 * kNG) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
+                        pol_first);
+        }
+#else
         named_bar(1 + wg, kGW * 32);   // the block is consumed: refill it
         if (leader && rb + 2 * kNG < bend) {
           refill_fence();
@@ -382,6 +401,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
           bulk_g2s_hint(gb + buf * kHalf, Tp + (size_t)(rb + 2 * kNG) * kHalf, kHalfBytes, &s_bar[wg][1 + buf],
                         pol_first);
         }
+#endif
         compare_fft<R>(v, xbuf, twr, lane);
         argmax_update<R>(v, 8 * rb + 2 * gi, lane, m, idx, ss);
       }
