@@ -58,7 +58,7 @@ __host__ __device__ constexpr int cta_warps(int R) { return 8 / (32 / R); }
 __host__ __device__ constexpr int xpose_size(int R) { return R * R; }   // XOR-swizzled transpose buffer
 // Row-phase buffer release by counted arrival (1) or a group barrier (0).
 #ifndef PCE_ROW_ARRIVE
-#define PCE_ROW_ARRIVE 0
+#define PCE_ROW_ARRIVE 1
 #endif
 template <int R>
 __device__ __forceinline__ void compare_fft(float2 (&v)[R], float2* xbuf, const float2 (&w)[R], int lane) {

@@ -278,6 +278,10 @@ __device__ __noinline__ float window_rows(const float2* blk, int ra, int rstart,
 // unit per warp group refilled after a group barrier (0).  Same box at N = 512:
 // with the scalar DIF FFT the group form won (80.2k vs 74.4k pairs/s); with the
 // DIT FFMA2 butterflies the per-warp form wins (90.1k vs 89.0k at a 75 MHz lower clock).
+// Row-phase half release by counted arrival (1) or a group barrier (0).
+#ifndef PCE2K_ROW_ARRIVE
+#define PCE2K_ROW_ARRIVE 1
+#endif
 #ifndef PCE2K_WARP_COLS
 #define PCE2K_WARP_COLS 1
 #endif
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
   float2* tw = smem + 4 * kUnitF2;                       // R*R twiddles (W_1024)
   float2* xbufs = tw + R * R;                            // one padded transpose buffer per warp
   __shared__ __align__(8) uint64_t s_bar[2][3];          // per group: column units, row halves even / odd
+  __shared__ unsigned s_done[2][2];                      // per group and row half: warps done reading
   __shared__ __align__(8) uint64_t s_wbar;
   __shared__ __align__(8) uint64_t s_cbar[kWarps];        // per warp: its column (PCE2K_WARP_COLS)
   __shared__ float s_v[kWarps];
@@ -319,6 +324,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
       for (int b = 0; b < 3; ++b) mbar_init(&s_bar[w][b], 1);
     mbar_init(&s_wbar, 1);
     for (int w = 0; w < kWarps; ++w) mbar_init(&s_cbar[w], 1);
+    s_done[0][0] = s_done[0][1] = s_done[1][0] = s_done[1][1] = 0u;
   }
   uint32_t ph = 0, wph = 0;
 #if PCE2K_WARP_COLS
@@ -454,6 +460,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         bulk_g2s_hint(gb + half * kUnitF2, Tp + ((size_t)rb * 2 + half) * kUnitF2, kUnitBytes,
                       &s_bar[wg][1 + half], pol_first);
       };
+      // a half is consumed once the group's kGW warps have read their row pair: the
+      // last reader (acq_rel count, PCE2K_ROW_ARRIVE) or the group leader after a
+      // group barrier refills it, behind the generic -> async proxy fence
+      auto release_half = [&](int rb, int half) {
+#if PCE2K_ROW_ARRIVE
+        __syncwarp();
+        if (lane == 0 && rb + 2 < kBlocks &&
+            atom_acq_rel_add_shared(&s_done[wg][half], 1u) % kGW == (unsigned)(kGW - 1)) {
+          refill_fence();
+          issue(rb + 2, half);
+        }
+#else
+        named_bar(1 + wg, kGW * 32);
+        if (leader && rb + 2 < kBlocks) {
+          refill_fence();
+          issue(rb + 2, half);
+        }
+#endif
+      };
       if (leader) {
         fence_proxy_async();   // T's generic-proxy stores (ordered by the barrier) -> async proxy
         issue(wg, 0);
@@ -465,20 +490,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
         mbar_wait(&s_bar[wg][1], (ph >> 1) & 1u);
         ph ^= 2u;
         block8_rows_z<R>(e, gb, gi, lane);
-        named_bar(1 + wg, kGW * 32);
-        if (leader && rb + 2 < kBlocks) {
-          refill_fence();   // the group's generic reads of this buffer before the async refill
-          issue(rb + 2, 0);
-        }
+        release_half(rb, 0);
         PCE2K_FFT(e);
         mbar_wait(&s_bar[wg][2], (ph >> 2) & 1u);
         ph ^= 4u;
         half_rows_zodd(o, gb + kUnitF2, gi, lane);
-        named_bar(1 + wg, kGW * 32);
-        if (leader && rb + 2 < kBlocks) {
-          refill_fence();
-          issue(rb + 2, 1);
-        }
+        release_half(rb, 1);
         PCE2K_FFT(o);
         radix2_last<true>(e, o, wl);
         argmax2k_update(e, o, 8 * rb + 2 * gi, lane, m, idx, ss);
