@@ -16,8 +16,9 @@
 //
 // Compare kernel (pce_cluster<R, CL>, CL = 1 in production): persistent, one
 // CTA = one SM per pair in flight (148 pairs); its 8 warps form two
-// independent warp groups (named barriers), each feeding itself through its own
-// bulk-copy (TMA 1-D) + mbarrier pipeline.  The 2-D inverse FFT needs one global
+// independent warp groups, each feeding itself through its own bulk-copy
+// (TMA 1-D) + mbarrier pipeline (per-warp column slices; row blocks released by
+// counted arrival); a grid round barrier keeps the in-flight pairs in step.  The 2-D inverse FFT needs one global
 // transpose; its intermediate T (4 MiB per pair at 1024^2) goes to a per-CTA
 // slot in HBM.  Per pair:
 //   column phase  per 4-column slice of X and Y (refilled as soon as the products
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
     PCE_PROBE(0);
 
     // ---------------- column phase ----------------
-    // Two warp groups run independently (named barriers), each streaming 4-column
+    // Two warp groups run independently, each streaming 4-column
     // slices of X and Y (contiguous in the slots) through its own buffer; a slice
     // is refilled as soon as the group has formed its products, so the copy lands
     // while the FFTs run, and the two groups' smem-heavy and FMA-heavy steps interleave.
