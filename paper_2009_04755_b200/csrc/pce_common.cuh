@@ -89,7 +89,10 @@ __device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk,
 // the same time and share them through L2 instead of drifting apart.  It is a
 // timing barrier only: a CTA stops waiting after kRoundSpin cycles, so partial
 // residency (another kernel holding SMs) can slow it but never deadlock it.
-constexpr long long kRoundSpin = 200000;
+#ifndef PCE_ROUND_SPIN
+#define PCE_ROUND_SPIN 200000
+#endif
+constexpr long long kRoundSpin = PCE_ROUND_SPIN;
 __device__ __forceinline__ void round_wait(const unsigned* rounds, int pi, int G, int tid) {
   if (rounds == nullptr || pi < G) return;
   if (tid == 0) {
