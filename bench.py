@@ -986,7 +986,7 @@ def main_pce(args, rank, world, local_rank):
                     "pairs_per_launch": batch, "ms_per_launch": per_launch_ms, "launches_sampled": ksamples,
                     "alg_bytes_per_pair": alg_bytes_per_pair, "peak_source": peaks_src,
                     "fp32_flops_per_pair": 2 * 5 * (side // 2) * side * math.log2(side),
-                    "grid": {"round_barrier": os.environ.get("RK_PCE_LOCKSTEP", "1") != "0",
+                    "grid": {"round_barrier": os.environ.get("RK_PCE_LOCKSTEP", "1") != "0" and side >= 1024,
                              "l2opts": int(os.environ.get("RK_PCE_L2OPTS", "3" if side == 2048 else "0")),
                              "what": "persistent-grid round barrier and L2 hints (bit 0 T evict_first, "
                                      "bit 1 spectra evict_last) the compare kernel ran with"}}
