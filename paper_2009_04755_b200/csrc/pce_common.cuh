@@ -93,10 +93,15 @@ __device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk,
 #define PCE_ROUND_SPIN 200000
 #endif
 constexpr long long kRoundSpin = PCE_ROUND_SPIN;
+#ifndef PCE_ROUND_SLACK_PCT
+#define PCE_ROUND_SLACK_PCT 0
+#endif
 __device__ __forceinline__ void round_wait(const unsigned* rounds, int pi, int G, int tid) {
   if (rounds == nullptr || pi < G) return;
   if (tid == 0) {
-    const unsigned target = (unsigned)(pi / G) * (unsigned)G;   // arrivals of rounds 0 .. k-1
+    // arrivals of rounds 0 .. k-1, less a slack of PCE_ROUND_SLACK_PCT % of the grid
+    const unsigned slack = (unsigned)(G * PCE_ROUND_SLACK_PCT / 100);
+    const unsigned target = (unsigned)(pi / G) * (unsigned)G - slack;
     const long long t0 = clock64();
     while (ld_acquire(rounds) < target && clock64() - t0 < kRoundSpin) __nanosleep(64);
   }
