@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(cta_warps(R) * 32, 1) pce_cluster(
   cluster_sync();
 
   for (int pi = cid; pi < job.npairs; pi += ncl) {
-    if (CL == 1) round_wait(rounds, pi, ncl, tid);
+    if (CL == 1) round_wait(rounds, pi, ncl, tid, PCE_ROUND_SLACK_PCT);
     const DevPair pr = job.pairs[pi];
     float2 v[R];
     PCE_PROBE(0);

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) pce2k_pair(const PairJob job, 
   const uint64_t pol_T = (l2opts & 1) ? pol_first : l2_policy_evict_normal();
 
   for (int pi = blockIdx.x; pi < job.npairs; pi += gridDim.x) {
-    round_wait(rounds, pi, gridDim.x, tid);
+    round_wait(rounds, pi, gridDim.x, tid, PCE2K_ROUND_SLACK_PCT);
     const DevPair pr = job.pairs[pi];
     const float2* Xs = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_a * slot_stride);
     const float2* Ys = reinterpret_cast<const float2*>(slots + (size_t)pr.slot_b * slot_stride);

@@ -93,14 +93,20 @@ __device__ __forceinline__ void block8_rows_z(float2 (&v)[R], const float2* blk,
 #define PCE_ROUND_SPIN 200000
 #endif
 constexpr long long kRoundSpin = PCE_ROUND_SPIN;
+// Round-barrier slack, % of the grid (measured: 10 at 1024^2 +0.6 %;
+// at 2048^2 any slack loses L2 reuse: 0).
 #ifndef PCE_ROUND_SLACK_PCT
-#define PCE_ROUND_SLACK_PCT 0
+#define PCE_ROUND_SLACK_PCT 10
 #endif
-__device__ __forceinline__ void round_wait(const unsigned* rounds, int pi, int G, int tid) {
+#ifndef PCE2K_ROUND_SLACK_PCT
+#define PCE2K_ROUND_SLACK_PCT 0
+#endif
+__device__ __forceinline__ void round_wait(const unsigned* rounds, int pi, int G, int tid, int slack_pct) {
   if (rounds == nullptr || pi < G) return;
   if (tid == 0) {
-    // arrivals of rounds 0 .. k-1, less a slack of PCE_ROUND_SLACK_PCT % of the grid
-    const unsigned slack = (unsigned)(G * PCE_ROUND_SLACK_PCT / 100);
+    // arrivals of rounds 0 .. k-1, less a slack of slack_pct % of the grid (a CTA
+    // may start round k while the last few CTAs finish round k-1)
+    const unsigned slack = (unsigned)(G * slack_pct / 100);
     const unsigned target = (unsigned)(pi / G) * (unsigned)G - slack;
     const long long t0 = clock64();
     while (ld_acquire(rounds) < target && clock64() - t0 < kRoundSpin) __nanosleep(64);
