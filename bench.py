@@ -604,6 +604,16 @@ def calibrate_ncc(args, params_fn, side, cameras, seed):
     return t_pre / m, t_cmp
 
 
+def leaf_ordered_pairs(m, leaf):
+    """All (i, j), i < j < m, in leaf order: leaf x leaf blocks of the upper
+    triangle (block rows, then block columns), pairs row-major inside a block."""
+    lb = max(1, int(leaf))
+    pairs = [(i, j) for bi in range(0, m, lb) for bj in range(bi, m, lb)
+             for i in range(bi, min(bi + lb, m)) for j in range(max(bj, i + 1), min(bj + lb, m))]
+    assert len(pairs) == m * (m - 1) // 2
+    return pairs
+
+
 def calibrate_pce(args, params_fn, side, cameras, seed):
     """Isolated single-GPU stage costs for the perf model (perfmodel.py:99-114):
     t_pre = preprocess time per item, t_cmp = compare time per pair, each from
@@ -623,10 +633,7 @@ def calibrate_pce(args, params_fn, side, cameras, seed):
     # pairs in the engine's leaf order (leaf_block x leaf_block blocks of the
     # triangle, pairs row-major inside a block): a round of the persistent compare
     # grid then draws on as few spectra as it does in a job
-    lb = max(1, args.leaf)
-    plist = [(i, j, i, j) for bi in range(0, m, lb) for bj in range(bi, m, lb)
-             for i in range(bi, min(bi + lb, m)) for j in range(max(bj, i + 1), min(bj + lb, m))]
-    assert len(plist) == m * (m - 1) // 2
+    plist = [(i, j, i, j) for i, j in leaf_ordered_pairs(m, args.leaf)]
     pairs = (_lib.Pair * len(plist))(*[_lib.Pair(*p) for p in plist])   # built once: no host gaps
     out = torch.zeros(m * (m - 1) // 2, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()

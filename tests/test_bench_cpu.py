@@ -42,3 +42,17 @@ def test_reference_arm_line_keeps_the_contract():
 def test_world_size_must_match_gpus():
     p = _run(["--gpus", "1"], env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"}, timeout=120)
     assert p.returncode == 2 and "WORLD_SIZE" in p.stderr
+
+
+def test_calibration_pairs_cover_the_triangle_once_in_leaf_order():
+    """The perf-model calibration lists every pair of its items exactly once, in
+    the engine's leaf order: leaf x leaf blocks, a block's pairs contiguous."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for m, leaf in ((64, 8), (64, 16), (37, 8), (10, 3), (5, 1)):
+        pairs = bench.leaf_ordered_pairs(m, leaf)
+        assert len(pairs) == len(set(pairs)) == m * (m - 1) // 2
+        assert all(0 <= i < j < m for i, j in pairs)
+        blocks = [(i // leaf, j // leaf) for i, j in pairs]
+        runs = [b for k, b in enumerate(blocks) if k == 0 or b != blocks[k - 1]]
+        assert len(runs) == len(set(runs))      # each block appears as one contiguous run
